@@ -1,0 +1,130 @@
+/*
+ * dmlp.h -- C-ABI of libdmlp.so, the sm_100a implementation of the on-line
+ * back-propagation / deformation / evaluation hot path of the reference
+ * package deepmlp (/root/reference/pkg/src/deepmlp).
+ *
+ * Plain pointers and sizes only.  Device pointers are CUDA device addresses
+ * (e.g. torch.Tensor.data_ptr()); "host or device" pointers are resolved by
+ * UVA (cudaMemcpyDefault).  Every call returns a status code; on failure
+ * dmlp_last_error() returns a thread-local message.
+ *
+ * Status codes map to the reference's Python exceptions:
+ *   DMLP_ESIZE  -> network.SizeMismatch      (network.py:20-21)
+ *   DMLP_EINVAL -> ValueError / deform.InvalidSigma / deform.EvenSize
+ *                  (kernels.py:289-290, deform.py:26-31, 51-62)
+ *   DMLP_ECUDA  -> RuntimeError (CUDA failure)
+ */
+#ifndef DMLP_H
+#define DMLP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DMLP_OK 0
+#define DMLP_ESIZE 1
+#define DMLP_EINVAL 2
+#define DMLP_ECUDA 3
+#define DMLP_ENCCL 4
+
+/* Weight residency of the persistent training kernel. */
+#define DMLP_RES_AUTO 0   /* smem-resident when the net fits on chip, else L2-streamed */
+#define DMLP_RES_L2 1     /* weights in HBM, L2-persisting window, streamed every sample */
+#define DMLP_RES_SMEM 2   /* every CTA keeps its owned rows in shared memory */
+
+typedef struct dmlp_net dmlp_net;
+
+/* deform.DeformParams (deform.py:40-62). */
+typedef struct {
+  double sigma_lo, sigma_hi;
+  double alpha_lo, alpha_hi;
+  double beta_default, beta_reduced;
+  double gamma_lo, gamma_hi;
+  int32_t kernel_size;
+} dmlp_deform_params;
+
+/* Thread-local description of the last failure ("" when none). */
+const char *dmlp_last_error(void);
+
+/* Library / device facts: SM count, max opt-in smem per block, L2 bytes. */
+int dmlp_device_info(int device, int32_t *n_sms, int32_t *smem_per_block,
+                     int64_t *l2_bytes, int64_t *persisting_l2_max);
+
+/* ---- network state (replaces network.Mlp / Architecture, network.py:40-106) ---- */
+
+/* sizes = Architecture.layer_sizes (input first).  n_ctas <= 0 selects one
+ * CTA per SM.  Weights are zero until dmlp_net_set_layer. */
+int dmlp_net_create(int device, const int32_t *sizes, int32_t n_sizes, int32_t residency,
+                    int32_t n_ctas, dmlp_net **out);
+int dmlp_net_destroy(dmlp_net *net);
+/* Residency actually selected, CTA count, threads per CTA, dynamic smem bytes. */
+int dmlp_net_info(dmlp_net *net, int32_t *residency, int32_t *n_ctas, int32_t *threads,
+                  int32_t *smem_bytes);
+
+/* Pack one layer from the reference layout (fo, fi+1) row-major, bias last
+ * (network.py:61-64), host or device pointer, n = fo*(fi+1) floats. */
+int dmlp_net_set_layer(dmlp_net *net, int32_t layer, const float *w, int64_t n);
+/* Unpack one layer back into the reference layout (host or device pointer). */
+int dmlp_net_get_layer(dmlp_net *net, int32_t layer, float *w, int64_t n);
+
+/* In-kernel profile of the persistent training kernel: when enabled, every
+ * CTA accumulates the cycles of its sample loop and the cycles spent in the
+ * inter-CTA exchange waits.  read returns the sums over CTAs and resets. */
+int dmlp_net_profile(dmlp_net *net, int32_t enable);
+int dmlp_net_read_profile(dmlp_net *net, int64_t *loop_cycles, int64_t *exchange_cycles);
+
+/* ---- on-line training (kernels.train_step / trainer.train_epoch) ---- */
+
+/* kernels.train_step (kernels.py:329-361): one on-line update on input x
+ * (n_inputs floats, host or device), target class digit, rate eta >= 0.
+ * y_out (10 floats, host or device) receives the output activations
+ * computed before the update.  Synchronous. */
+int dmlp_train_step(dmlp_net *net, const float *x, int32_t digit, float eta, float *y_out);
+
+/* trainer.train_epoch (trainer.py:104-123): sequential on-line pass over
+ * samples order[0..n) (order NULL = identity) of x_dev (rows of n_inputs
+ * floats, row stride ldx floats) with labels_dev (u8).  Adds the number of
+ * argmax errors to *wrong_dev (device int64).  y_last_dev (optional, 10
+ * floats) receives the output of the last sample.  Asynchronous on stream. */
+int dmlp_train_epoch(dmlp_net *net, const float *x_dev, int64_t ldx, const uint8_t *labels_dev,
+                     const int32_t *order_dev, int64_t n, float eta, int64_t *wrong_dev,
+                     float *y_last_dev, void *stream);
+
+/* ---- evaluation (network.forward_batch / eval_report.evaluate) ---- */
+
+/* network.forward_batch (network.py:118-130): out_dev (n,10) = outputs. */
+int dmlp_forward_batch(dmlp_net *net, const float *x_dev, int64_t n, float *out_dev,
+                       void *stream);
+
+/* trainer.error_percent + eval_report.evaluate counting (trainer.py:90-96,
+ * eval_report.py:36-67): counts_dev (int64[102]) += {wrong, confusion[10][10]
+ * (rows = true digit), second_guess_correct}; guess_dev (optional, int32
+ * (n,2)) = top-2 ranked digits (stable: ties go to the smaller digit). */
+int dmlp_eval_counts(dmlp_net *net, const float *x_dev, const uint8_t *labels_dev, int64_t n,
+                     int64_t *counts_dev, int32_t *guess_dev, void *stream);
+
+/* ---- deformation (deform.py / rng.py) ---- */
+
+/* deform.deform_epoch (deform.py:217-247) for images [first, first+n) of a
+ * split: raw_dev (n,28,28) u8, labels_dev (n) u8 -> out_dev (n,29,29) f32.
+ * Image i uses substream(seed, 2, epoch, first+i) (rng.py:27-38). */
+int dmlp_deform(const uint8_t *raw_dev, const uint8_t *labels_dev, int64_t first, int64_t n,
+                uint64_t seed, uint64_t epoch, const dmlp_deform_params *params,
+                float *out_dev, void *stream);
+
+/* Injected-field parity mode: the random draws are supplied.
+ * noise_dx_dev / noise_dy_dev: (n,29,29) f64; scalars_dev: (n,6) f64 =
+ * sigma, alpha, mode (0 rotation, 1 shear), angle (deg), sx, sy. */
+int dmlp_deform_injected(const uint8_t *raw_dev, int64_t n, const double *noise_dx_dev,
+                         const double *noise_dy_dev, const double *scalars_dev,
+                         int32_t kernel_size, float *out_dev, void *stream);
+
+/* deform.upscale_dataset (deform.py:250-257): (n,28,28) u8 -> (n,841) f32. */
+int dmlp_upscale(const uint8_t *raw_dev, int64_t n, float *out_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,424 @@
+// capi.cu -- the extern "C" boundary of libdmlp.so (see include/dmlp.h).
+//
+// Owns the network state that the reference keeps in network.Mlp
+// (network.py:87-106): device weights in the kernel's padded row layout,
+// the flag-word exchange buffers of the persistent kernel, and the sample
+// sequence counter that tags every exchanged word.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "dmlp_internal.h"
+
+namespace dmlp {
+
+static thread_local std::string g_err;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return DMLP_OK;
+  return set_error(DMLP_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define DMLP_CUDA(call)                                 \
+  do {                                                  \
+    int _rc = ::dmlp::cuda_check((call), #call);        \
+    if (_rc != DMLP_OK) return _rc;                     \
+  } while (0)
+
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Reference layout (fo, fi+1) row-major -> device rows of `pitch` floats,
+// replicated `copies` times (the output layer keeps one copy per CTA).
+__global__ void k_pack(const float* __restrict__ src, float* __restrict__ dst, int fo, int fi,
+                       int pitch, int copies) {
+  const long long per = (long long)fo * pitch;
+  const long long total = per * copies;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t % per;
+    const int j = (int)(r / pitch), i = (int)(r % pitch);
+    dst[t] = (i <= fi) ? src[(long long)j * (fi + 1) + i] : 0.0f;
+  }
+}
+
+__global__ void k_unpack(const float* __restrict__ src, float* __restrict__ dst, int fo, int fi,
+                         int pitch) {
+  const long long total = (long long)fo * (fi + 1);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(t / (fi + 1)), i = (int)(t % (fi + 1));
+    dst[t] = src[(long long)j * pitch + i];
+  }
+}
+
+static int own_max_rows(int fo, int nct) {
+  int m = 0;
+  for (int c = 0; c < nct; c++) {
+    const int r0 = (int)((long long)fo * c / nct), r1 = (int)((long long)fo * (c + 1) / nct);
+    if (r1 - r0 > m) m = r1 - r0;
+  }
+  return m;
+}
+
+// Lay out dynamic shared memory; returns bytes.
+static int layout_smem(dmlp_net* net, bool resident) {
+  NetDev& d = net->dev;
+  const int L = d.L;
+  int off = 0;
+  auto take = [&](int floats) {
+    const int o = off;
+    off += round_up(floats, 4);
+    return o;
+  };
+  d.in0_off[0] = take(d.ly[0].pitch);
+  d.in0_off[1] = take(d.ly[0].pitch);
+  for (int l = 1; l < L; l++) d.ly[l].in_off = take(d.ly[l].pitch);
+  d.ly[0].in_off = d.in0_off[0];
+  int maxr = 1;
+  for (int l = 0; l < L - 1; l++) {
+    const int r = own_max_rows(d.ly[l].fo, d.nct);
+    d.ly[l].t_off = take(r);
+    if (r > maxr) maxr = r;
+  }
+  d.ly[L - 1].t_off = 0;
+  for (int b = 0; b < 2; b++) {
+    d.delta_off[b] = take(maxr);
+    d.dsc_off[b] = take(maxr);
+  }
+  d.red_off = take(kWarps * 32);
+  d.out_off = take(4 * kMaxOut);
+  d.wsm_off = off;
+  if (resident) {
+    int w = 0;
+    for (int l = 0; l < L; l++) {
+      const int r = (l < L - 1) ? own_max_rows(d.ly[l].fo, d.nct) : d.ly[l].fo;
+      w += r * d.ly[l].pitch;
+    }
+    take(w);
+  }
+  return off * (int)sizeof(float);
+}
+
+}  // namespace dmlp
+
+using namespace dmlp;
+
+extern "C" {
+
+const char* dmlp_last_error(void) { return g_err.c_str(); }
+
+int dmlp_device_info(int device, int32_t* n_sms, int32_t* smem_per_block, int64_t* l2_bytes,
+                     int64_t* persisting_l2_max) {
+  cudaDeviceProp p;
+  DMLP_CUDA(cudaGetDeviceProperties(&p, device));
+  if (n_sms) *n_sms = p.multiProcessorCount;
+  if (smem_per_block) *smem_per_block = (int32_t)p.sharedMemPerBlockOptin;
+  if (l2_bytes) *l2_bytes = p.l2CacheSize;
+  if (persisting_l2_max) *persisting_l2_max = p.persistingL2CacheMaxSize;
+  return DMLP_OK;
+}
+
+int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t residency,
+                    int32_t n_ctas, dmlp_net** out) {
+  if (!out || !sizes) return set_error(DMLP_EINVAL, "null argument");
+  *out = nullptr;
+  if (n_sizes < 2) return set_error(DMLP_EINVAL, "architecture needs at least input and output sizes");
+  if (n_sizes - 1 > kMaxLayers)
+    return set_error(DMLP_EINVAL, "at most %d weight layers supported, got %d", kMaxLayers,
+                     n_sizes - 1);
+  for (int i = 0; i < n_sizes; i++)
+    if (sizes[i] < 1) return set_error(DMLP_EINVAL, "layer sizes must be positive");
+  if (sizes[n_sizes - 1] > kMaxOut)
+    return set_error(DMLP_EINVAL, "output layer wider than %d is not supported", kMaxOut);
+  if (residency < DMLP_RES_AUTO || residency > DMLP_RES_SMEM)
+    return set_error(DMLP_EINVAL, "unknown residency %d", residency);
+  DMLP_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  DMLP_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return set_error(DMLP_ECUDA, "device %d is sm_%d%d; libdmlp is built for sm_100a", device,
+                     prop.major, prop.minor);
+
+  dmlp_net* net = new dmlp_net();
+  net->device = device;
+  net->n_sizes = n_sizes;
+  memcpy(net->sizes, sizes, sizeof(int32_t) * n_sizes);
+  NetDev& d = net->dev;
+  d.L = n_sizes - 1;
+  int nct = n_ctas > 0 ? n_ctas : prop.multiProcessorCount;
+  if (nct > prop.multiProcessorCount) nct = prop.multiProcessorCount;
+  for (int l = 0; l < d.L; l++)  // every CTA must own at least one row of every hidden layer
+    if (l < d.L - 1 && sizes[l + 1] < nct) nct = sizes[l + 1];
+  d.nct = nct;
+
+  size_t woff = 0;
+  for (int l = 0; l < d.L; l++) {
+    HostLayer& h = net->hl[l];
+    h.fi = sizes[l];
+    h.fo = sizes[l + 1];
+    h.pitch = round_up(h.fi + 1, 4);
+    h.copies = (l == d.L - 1) ? (size_t)nct : 1;
+    h.w_off = woff;
+    woff += (size_t)h.fo * h.pitch * h.copies;
+    d.ly[l].fi = h.fi;
+    d.ly[l].fo = h.fo;
+    d.ly[l].pitch = h.pitch;
+  }
+  net->w_floats = woff;
+
+  // exchange buffers: y words [2][fo] for hidden layers, partial words [2][nct][pitch] for l>=1
+  size_t ll = 0;
+  size_t yoff[kMaxLayers], poff[kMaxLayers];
+  for (int l = 0; l < d.L - 1; l++) {
+    yoff[l] = ll;
+    ll += 2 * (size_t)d.ly[l].fo;
+    if (l >= 1) {
+      poff[l] = ll;
+      ll += 2 * (size_t)nct * d.ly[l].pitch;
+    }
+  }
+  net->ll_words = ll;
+
+  // residency
+  int smem_l2 = layout_smem(net, false);
+  int smem_res = layout_smem(net, true);
+  const int smem_cap = (int)prop.sharedMemPerBlockOptin;
+  int res = residency;
+  if (res == DMLP_RES_AUTO) res = (smem_res <= smem_cap) ? DMLP_RES_SMEM : DMLP_RES_L2;
+  if (res == DMLP_RES_SMEM && smem_res > smem_cap) {
+    delete net;
+    return set_error(DMLP_EINVAL,
+                     "net does not fit in shared memory: %d bytes per CTA needed, %d available",
+                     smem_res, smem_cap);
+  }
+  if (smem_l2 > smem_cap) {
+    delete net;
+    return set_error(DMLP_EINVAL, "activation vectors need %d bytes of shared memory (> %d)",
+                     smem_l2, smem_cap);
+  }
+  net->residency = res;
+  d.resident = (res == DMLP_RES_SMEM) ? 1 : 0;
+  net->smem_bytes = layout_smem(net, d.resident != 0);
+
+  int rc = DMLP_OK;
+  auto fail = [&](int code) {
+    dmlp_net_destroy(net);
+    return code;
+  };
+  if ((rc = cuda_check(set_train_attributes(net->smem_bytes), "cudaFuncSetAttribute")))
+    return fail(rc);
+  int bps = 0;
+  if ((rc = cuda_check(train_occupancy(net->smem_bytes, &bps), "occupancy"))) return fail(rc);
+  if (bps < 1)
+    return fail(set_error(DMLP_ECUDA, "persistent kernel cannot be resident (%d smem bytes)",
+                          net->smem_bytes));
+
+  if ((rc = cuda_check(cudaMalloc(&net->d_w, net->w_floats * sizeof(float)), "cudaMalloc weights")))
+    return fail(rc);
+  if ((rc = cuda_check(cudaMemset(net->d_w, 0, net->w_floats * sizeof(float)), "memset")))
+    return fail(rc);
+  if (ll) {
+    if ((rc = cuda_check(cudaMalloc(&net->d_ll, ll * 8), "cudaMalloc exchange"))) return fail(rc);
+    if ((rc = cuda_check(cudaMemset(net->d_ll, 0, ll * 8), "memset"))) return fail(rc);
+  }
+  if ((rc = cuda_check(cudaMalloc(&net->d_err, sizeof(int)), "cudaMalloc"))) return fail(rc);
+  if ((rc = cuda_check(cudaMemset(net->d_err, 0, sizeof(int)), "memset"))) return fail(rc);
+  const int fi0 = sizes[0];
+  if ((rc = cuda_check(cudaMalloc(&net->d_stage, (fi0 + 64) * sizeof(float)), "cudaMalloc")))
+    return fail(rc);
+  if ((rc = cuda_check(cudaMalloc(&net->d_stage_lab, 64), "cudaMalloc"))) return fail(rc);
+  if ((rc = cuda_check(cudaMalloc(&net->d_stage_wrong, 64), "cudaMalloc"))) return fail(rc);
+  if ((rc = cuda_check(cudaStreamCreateWithFlags(&net->stream, cudaStreamNonBlocking),
+                       "cudaStreamCreate")))
+    return fail(rc);
+  for (int l = 0; l < d.L; l++) {
+    d.ly[l].w = net->d_w + net->hl[l].w_off;
+    d.ly[l].yll = (l < d.L - 1) ? net->d_ll + yoff[l] : nullptr;
+    d.ly[l].pll = (l >= 1 && l < d.L - 1) ? net->d_ll + poff[l] : nullptr;
+  }
+  d.err = net->d_err;
+  d.prof = nullptr;
+  *out = net;
+  return DMLP_OK;
+}
+
+int dmlp_net_destroy(dmlp_net* net) {
+  if (!net) return DMLP_OK;
+  cudaSetDevice(net->device);
+  if (net->stream) cudaStreamSynchronize(net->stream);
+  cudaFree(net->d_w);
+  cudaFree(net->d_ll);
+  cudaFree(net->d_err);
+  cudaFree(net->d_stage);
+  cudaFree(net->d_stage_lab);
+  cudaFree(net->d_stage_wrong);
+  cudaFree(net->d_act[0]);
+  cudaFree(net->d_act[1]);
+  cudaFree(net->dev.prof);
+  if (net->stream) cudaStreamDestroy(net->stream);
+  delete net;
+  return DMLP_OK;
+}
+
+int dmlp_net_info(dmlp_net* net, int32_t* residency, int32_t* n_ctas, int32_t* threads,
+                  int32_t* smem_bytes) {
+  if (!net) return set_error(DMLP_EINVAL, "null net");
+  if (residency) *residency = net->residency;
+  if (n_ctas) *n_ctas = net->dev.nct;
+  if (threads) *threads = kThreads;
+  if (smem_bytes) *smem_bytes = net->smem_bytes;
+  return DMLP_OK;
+}
+
+int dmlp_net_profile(dmlp_net* net, int32_t enable) {
+  if (!net) return set_error(DMLP_EINVAL, "null net");
+  DMLP_CUDA(cudaSetDevice(net->device));
+  DMLP_CUDA(cudaStreamSynchronize(net->stream));
+  if (enable && !net->dev.prof) {
+    unsigned long long* p = nullptr;
+    DMLP_CUDA(cudaMalloc(&p, 2 * sizeof(unsigned long long) * net->dev.nct));
+    DMLP_CUDA(cudaMemset(p, 0, 2 * sizeof(unsigned long long) * net->dev.nct));
+    net->dev.prof = p;
+  } else if (!enable && net->dev.prof) {
+    DMLP_CUDA(cudaDeviceSynchronize());
+    cudaFree(net->dev.prof);
+    net->dev.prof = nullptr;
+  }
+  return DMLP_OK;
+}
+
+int dmlp_net_read_profile(dmlp_net* net, int64_t* loop_cycles, int64_t* exchange_cycles) {
+  if (!net) return set_error(DMLP_EINVAL, "null net");
+  if (!net->dev.prof) return set_error(DMLP_EINVAL, "profiling is not enabled");
+  DMLP_CUDA(cudaSetDevice(net->device));
+  DMLP_CUDA(cudaDeviceSynchronize());
+  const int n = 2 * net->dev.nct;
+  unsigned long long* h = new unsigned long long[n];
+  cudaError_t e = cudaMemcpy(h, net->dev.prof, n * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    delete[] h;
+    return cuda_check(e, "cudaMemcpy profile");
+  }
+  long long a = 0, b = 0;
+  for (int c = 0; c < net->dev.nct; c++) {
+    a += (long long)h[2 * c];
+    b += (long long)h[2 * c + 1];
+  }
+  delete[] h;
+  if (loop_cycles) *loop_cycles = a;
+  if (exchange_cycles) *exchange_cycles = b;
+  DMLP_CUDA(cudaMemset(net->dev.prof, 0, n * sizeof(unsigned long long)));
+  return DMLP_OK;
+}
+
+int dmlp_net_set_layer(dmlp_net* net, int32_t layer, const float* w, int64_t n) {
+  if (!net || !w) return set_error(DMLP_EINVAL, "null argument");
+  if (layer < 0 || layer >= net->dev.L) return set_error(DMLP_EINVAL, "layer %d out of range", layer);
+  const HostLayer& h = net->hl[layer];
+  if (n != (int64_t)h.fo * (h.fi + 1))
+    return set_error(DMLP_ESIZE, "layer %d holds %lld weights, got %lld", layer,
+                     (long long)h.fo * (h.fi + 1), (long long)n);
+  DMLP_CUDA(cudaSetDevice(net->device));
+  float* tmp = nullptr;
+  DMLP_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), net->stream));
+  DMLP_CUDA(cudaMemcpyAsync(tmp, w, n * sizeof(float), cudaMemcpyDefault, net->stream));
+  k_pack<<<296, 256, 0, net->stream>>>(tmp, net->d_w + h.w_off, h.fo, h.fi, h.pitch,
+                                       (int)h.copies);
+  DMLP_CUDA(cudaGetLastError());
+  DMLP_CUDA(cudaFreeAsync(tmp, net->stream));
+  DMLP_CUDA(cudaStreamSynchronize(net->stream));
+  return DMLP_OK;
+}
+
+int dmlp_net_get_layer(dmlp_net* net, int32_t layer, float* w, int64_t n) {
+  if (!net || !w) return set_error(DMLP_EINVAL, "null argument");
+  if (layer < 0 || layer >= net->dev.L) return set_error(DMLP_EINVAL, "layer %d out of range", layer);
+  const HostLayer& h = net->hl[layer];
+  if (n != (int64_t)h.fo * (h.fi + 1))
+    return set_error(DMLP_ESIZE, "layer %d holds %lld weights, got %lld", layer,
+                     (long long)h.fo * (h.fi + 1), (long long)n);
+  DMLP_CUDA(cudaSetDevice(net->device));
+  float* tmp = nullptr;
+  DMLP_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), net->stream));
+  k_unpack<<<296, 256, 0, net->stream>>>(net->d_w + h.w_off, tmp, h.fo, h.fi, h.pitch);
+  DMLP_CUDA(cudaGetLastError());
+  DMLP_CUDA(cudaMemcpyAsync(w, tmp, n * sizeof(float), cudaMemcpyDefault, net->stream));
+  DMLP_CUDA(cudaFreeAsync(tmp, net->stream));
+  DMLP_CUDA(cudaStreamSynchronize(net->stream));
+  return DMLP_OK;
+}
+
+static int check_kernel_error(dmlp_net* net, cudaError_t e) {
+  if (e != cudaSuccess) {
+    int flag = 0;
+    cudaMemcpy(&flag, net->d_err, sizeof(int), cudaMemcpyDeviceToHost);
+    return set_error(DMLP_ECUDA, "training kernel failed: %s%s", cudaGetErrorString(e),
+                     flag ? " (exchange wait timed out)" : "");
+  }
+  return DMLP_OK;
+}
+
+static int run_epoch(dmlp_net* net, const float* x, long long ldx, const uint8_t* labels,
+                     const int32_t* order, long long n, float eta, long long* wrong, float* y_last,
+                     cudaStream_t st) {
+  if (n <= 0) return DMLP_OK;
+  if (!(eta >= 0.0f)) return set_error(DMLP_EINVAL, "eta must be non-negative");
+  if (ldx < net->sizes[0]) return set_error(DMLP_ESIZE, "row stride %lld < fan-in %d", ldx,
+                                            net->sizes[0]);
+  if ((unsigned long long)net->seq + (unsigned long long)n >= 0xFFFFFFF0ull) {
+    // flag wrap-around: clear the exchange words and restart the sequence
+    DMLP_CUDA(cudaStreamSynchronize(st));
+    if (net->d_ll) DMLP_CUDA(cudaMemset(net->d_ll, 0, net->ll_words * 8));
+    DMLP_CUDA(cudaDeviceSynchronize());
+    net->seq = 1;
+  }
+  const uint32_t seq0 = net->seq;
+  cudaError_t e = launch_train(net, x, ldx, labels, order, n, eta, seq0, wrong, y_last, st);
+  if (e != cudaSuccess) return check_kernel_error(net, e);
+  net->seq += (uint32_t)n;
+  return DMLP_OK;
+}
+
+int dmlp_train_step(dmlp_net* net, const float* x, int32_t digit, float eta, float* y_out) {
+  if (!net || !x) return set_error(DMLP_EINVAL, "null argument");
+  const int nout = net->sizes[net->n_sizes - 1];
+  if (digit < 0 || digit >= nout) return set_error(DMLP_EINVAL, "digit %d out of range", digit);
+  DMLP_CUDA(cudaSetDevice(net->device));
+  const int fi0 = net->sizes[0];
+  uint8_t lab = (uint8_t)digit;
+  DMLP_CUDA(cudaMemcpyAsync(net->d_stage, x, fi0 * sizeof(float), cudaMemcpyDefault, net->stream));
+  DMLP_CUDA(cudaMemcpyAsync(net->d_stage_lab, &lab, 1, cudaMemcpyHostToDevice, net->stream));
+  float* ydev = net->d_stage + round_up(fi0, 32);
+  int rc = run_epoch(net, net->d_stage, fi0, net->d_stage_lab, nullptr, 1, eta, nullptr, ydev,
+                     net->stream);
+  if (rc) return rc;
+  if (y_out)
+    DMLP_CUDA(cudaMemcpyAsync(y_out, ydev, nout * sizeof(float), cudaMemcpyDefault, net->stream));
+  return check_kernel_error(net, cudaStreamSynchronize(net->stream));
+}
+
+int dmlp_train_epoch(dmlp_net* net, const float* x_dev, int64_t ldx, const uint8_t* labels_dev,
+                     const int32_t* order_dev, int64_t n, float eta, int64_t* wrong_dev,
+                     float* y_last_dev, void* stream) {
+  if (!net || (!x_dev && n > 0) || (!labels_dev && n > 0))
+    return set_error(DMLP_EINVAL, "null argument");
+  DMLP_CUDA(cudaSetDevice(net->device));
+  return run_epoch(net, x_dev, ldx, labels_dev, order_dev, n, eta, (long long*)wrong_dev,
+                   y_last_dev, (cudaStream_t)stream);
+}
+
+}  // extern "C"

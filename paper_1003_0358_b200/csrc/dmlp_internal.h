@@ -1,0 +1,83 @@
+// dmlp_internal.h -- shared host/device declarations of libdmlp.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/dmlp.h"
+
+namespace dmlp {
+
+constexpr int kThreads = 512;  // threads per CTA of the persistent kernel
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxLayers = 16;
+constexpr int kMaxOut = 32;  // replicated output layer: at most 32 classes
+
+// One weight layer as the persistent kernel sees it.
+struct LayerDev {
+  int fi, fo, pitch;     // fan-in, fan-out, floats per device row (>= fi+1, %4 == 0)
+  int in_off;            // smem offset (floats) of this layer's input vector (pitch long)
+  int t_off;             // smem offset of the owned rows' tanh(B*a) cache
+  float* w;              // [fo][pitch] (output layer: [nct][fo][pitch], one copy per CTA)
+  unsigned long long* yll;  // hidden: [2][fo] flag-carrying activations
+  unsigned long long* pll;  // hidden l>=1: [2][nct][pitch] flag-carrying column partials
+};
+
+struct NetDev {
+  int L;    // weight layers
+  int nct;  // CTAs (row owners)
+  int resident;  // 1: owned rows live in shared memory (DMLP_RES_SMEM)
+  int in0_off[2];
+  int delta_off[2];
+  int dsc_off[2];
+  int red_off;
+  int out_off;
+  int wsm_off;  // smem-resident weights region (floats)
+  int* err;
+  unsigned long long* prof;  // optional [nct][2] {loop cycles, exchange-wait cycles}
+  LayerDev ly[kMaxLayers];
+};
+
+struct HostLayer {
+  int fi, fo, pitch;
+  size_t w_off;  // float offset into the weights allocation
+  size_t copies; // 1, or nct for the replicated output layer
+};
+
+}  // namespace dmlp
+
+struct dmlp_net {
+  int device;
+  int residency;
+  int n_sizes;
+  int32_t sizes[dmlp::kMaxLayers + 1];
+  dmlp::HostLayer hl[dmlp::kMaxLayers];
+  dmlp::NetDev dev;
+  float* d_w = nullptr;
+  size_t w_floats = 0;
+  unsigned long long* d_ll = nullptr;
+  size_t ll_words = 0;
+  int* d_err = nullptr;
+  int smem_bytes = 0;
+  uint32_t seq = 1;  // next sample sequence number (flag value)
+  cudaStream_t stream = nullptr;
+  float* d_stage = nullptr;  // train_step staging: x, y
+  uint8_t* d_stage_lab = nullptr;
+  long long* d_stage_wrong = nullptr;
+  // evaluation scratch
+  float* d_act[2] = {nullptr, nullptr};
+  size_t act_rows = 0;
+  int act_ld = 0;
+};
+
+namespace dmlp {
+int set_error(int code, const char* fmt, ...);
+int cuda_check(cudaError_t e, const char* what);
+cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
+                         const uint8_t* labels, const int32_t* order, long long n, float eta,
+                         uint32_t seq0, long long* wrong, float* y_last, cudaStream_t st);
+int train_smem_bytes(const dmlp_net* net);
+cudaError_t set_train_attributes(int smem_bytes);
+cudaError_t train_occupancy(int smem_bytes, int* blocks_per_sm);
+}  // namespace dmlp

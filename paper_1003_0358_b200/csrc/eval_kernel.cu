@@ -1,0 +1,247 @@
+// eval_kernel.cu -- batched evaluation forward on sm_100a.
+//
+// Replaces network.forward_batch (network.py:118-130), rank_outputs
+// (network.py:133-135), trainer.error_percent (trainer.py:90-96) and the
+// counting of eval_report.evaluate (eval_report.py:36-67).
+//   * hidden layers: fp32 SIMT GEMM (128x128 CTA tile, 8x8 per thread,
+//     double-buffered smem) with the bias add and the scaled tanh fused in
+//     the epilogue.  fp32 accumulation keeps argmax parity with the
+//     reference's OpenBLAS sgemm; tensor-core tf32 would not.
+//   * output layer: one warp per sample (10 rows, weights in smem), fused
+//     with stable top-2 ranking and the {wrong, confusion, second-guess}
+//     counters (block-aggregated, one atomic per counter per CTA).
+// The samples are processed in chunks so the activation scratch stays
+// bounded; chunks reuse the net's scratch buffers.
+#include <cuda_runtime.h>
+
+#include "dmlp_internal.h"
+#include "dmlp_math.cuh"
+
+namespace dmlp {
+
+constexpr int BM = 128, BN = 128, BK = 16, GT = 256;
+
+// Y[m][j] = A*tanh(B*(sum_k X[m][k] W[j][k] + W[j][K])), m < M, j < N.
+__global__ void __launch_bounds__(GT)
+    k_gemm_tanh(const float* __restrict__ X, long long ldx, const float* __restrict__ W, int ldw,
+                int M, int N, int K, float* __restrict__ Y, int ldy) {
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
+  // loader mapping: 128 rows x 16 k = 2048 floats, 8 per thread: row = tid/2, k = (tid&1)*8 + e
+  const int lr = tid >> 1, lk = (tid & 1) * 8;
+  float ra[8], rb[8];
+  auto load = [&](int k0) {
+    const int m = bm + lr, j = bn + lr;
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int k = k0 + lk + e;
+      ra[e] = (m < M && k < K) ? X[(long long)m * ldx + k] : 0.0f;
+      rb[e] = (j < N && k < K) ? W[(long long)j * ldw + k] : 0.0f;
+    }
+  };
+  auto store = [&](int b) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      As[b][lk + e][lr] = ra[e];
+      Bs[b][lk + e][lr] = rb[e];
+    }
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
+  load(0);
+  store(0);
+  __syncthreads();
+  const int nk = (K + BK - 1) / BK;
+  for (int kt = 0; kt < nk; kt++) {
+    const int b = kt & 1;
+    if (kt + 1 < nk) load((kt + 1) * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk++) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[b][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[b][kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[b][kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[b][kk][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) {
+      store(b ^ 1);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int m = bm + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int n = bn + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (n >= N) continue;
+      const float a = acc[i][j] + W[(long long)n * ldw + K];
+      float t;
+      Y[(long long)m * ldy + n] = dev_scaled_tanh(a, &t);
+    }
+  }
+}
+
+constexpr int OT = 256;  // 8 warps, one sample per warp per iteration
+
+// Output layer + ranking + counts.  W: (nout, ldw) rows with bias at column K.
+__global__ void __launch_bounds__(OT)
+    k_out_rank(const float* __restrict__ X, long long ldx, const float* __restrict__ W, int ldw,
+               int M, int K, int nout, float* __restrict__ out, const uint8_t* __restrict__ labels,
+               unsigned long long* __restrict__ counts, int* __restrict__ guess) {
+  extern __shared__ __align__(16) float osm[];
+  float* Ws = osm;  // nout * ldw
+  unsigned* cnt = reinterpret_cast<unsigned*>(osm + nout * ldw);  // 102 counters
+  for (int i = threadIdx.x; i < nout * ldw; i += OT) Ws[i] = W[i];
+  for (int i = threadIdx.x; i < 102; i += OT) cnt[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int m = blockIdx.x * (OT / 32) + warp; m < M; m += gridDim.x * (OT / 32)) {
+    float acc[kMaxOut];
+#pragma unroll
+    for (int j = 0; j < kMaxOut; j++) acc[j] = 0.0f;
+    for (int k = lane; k < K; k += 32) {
+      const float x = X[(long long)m * ldx + k];
+#pragma unroll
+      for (int j = 0; j < kMaxOut; j++)
+        if (j < nout) acc[j] = fmaf(x, Ws[j * ldw + k], acc[j]);
+    }
+    float y[kMaxOut];
+#pragma unroll
+    for (int j = 0; j < kMaxOut; j++) {
+      if (j < nout) {
+        float s = acc[j];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        float t;
+        y[j] = dev_scaled_tanh(s + Ws[j * ldw + K], &t);
+      }
+    }
+    if (lane == 0) {
+      if (out)
+        for (int j = 0; j < nout; j++) out[(long long)m * nout + j] = y[j];
+      // stable argsort(-y): ties keep the smaller digit; NaN ranks last
+      int g1 = -1, g2 = -1;
+      for (int j = 0; j < nout; j++) {
+        const float v = y[j];
+        if (v != v) continue;
+        if (g1 < 0 || v > y[g1]) { g2 = g1; g1 = j; }
+        else if (g2 < 0 || v > y[g2]) { g2 = j; }
+      }
+      if (g1 < 0) { g1 = 0; g2 = nout > 1 ? 1 : 0; }
+      else if (g2 < 0) { g2 = (g1 == 0 && nout > 1) ? 1 : 0; }
+      if (guess) {
+        guess[2 * (long long)m] = g1;
+        guess[2 * (long long)m + 1] = g2;
+      }
+      if (labels && counts) {
+        const int t = labels[m];
+        if (g1 != t) {
+          atomicAdd(&cnt[0], 1u);
+          if (g2 == t) atomicAdd(&cnt[101], 1u);
+        }
+        if (t < 10 && g1 < 10) atomicAdd(&cnt[1 + t * 10 + g1], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (labels && counts)
+    for (int i = threadIdx.x; i < 102; i += OT)
+      if (cnt[i]) atomicAdd(&counts[i], (unsigned long long)cnt[i]);
+}
+
+static int ensure_act(dmlp_net* net, size_t rows, int ld) {
+  if (net->act_rows >= rows && net->act_ld >= ld) return DMLP_OK;
+  cudaFree(net->d_act[0]);
+  cudaFree(net->d_act[1]);
+  net->d_act[0] = net->d_act[1] = nullptr;
+  net->act_rows = 0;
+  for (int b = 0; b < 2; b++)
+    if (int rc = cuda_check(cudaMalloc(&net->d_act[b], rows * ld * sizeof(float)), "cudaMalloc"))
+      return rc;
+  net->act_rows = rows;
+  net->act_ld = ld;
+  return DMLP_OK;
+}
+
+static int run_eval(dmlp_net* net, const float* x, long long n, float* out, const uint8_t* labels,
+                    long long* counts, int* guess, cudaStream_t st) {
+  if (n <= 0) return DMLP_OK;
+  if (int rc = cuda_check(cudaSetDevice(net->device), "cudaSetDevice")) return rc;
+  const int L = net->dev.L;
+  int maxld = 4;  // activation row stride = input pitch of the consuming layer
+  for (int l = 1; l < L; l++) maxld = maxld > net->hl[l].pitch ? maxld : net->hl[l].pitch;
+  const long long chunk = n < 16384 ? n : 16384;
+  if (int rc = ensure_act(net, (size_t)chunk, maxld)) return rc;
+  const HostLayer& ho = net->hl[L - 1];
+  const int osmem = (ho.fo * ho.pitch + 128) * (int)sizeof(float);
+  if (int rc = cuda_check(
+          cudaFuncSetAttribute(k_out_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, osmem),
+          "cudaFuncSetAttribute"))
+    return rc;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, net->device);
+  for (long long m0 = 0; m0 < n; m0 += chunk) {
+    const int M = (int)((n - m0) < chunk ? (n - m0) : chunk);
+    const float* in = x + m0 * net->sizes[0];
+    long long ldin = net->sizes[0];
+    int b = 0;
+    for (int l = 0; l < L - 1; l++) {
+      const HostLayer& h = net->hl[l];
+      float* y = net->d_act[b];
+      const int ldy = net->hl[l + 1].pitch;
+      dim3 grid((h.fo + BN - 1) / BN, (M + BM - 1) / BM);
+      k_gemm_tanh<<<grid, GT, 0, st>>>(in, ldin, net->d_w + h.w_off, h.pitch, M, h.fo, h.fi, y,
+                                        ldy);
+      in = y;
+      ldin = ldy;
+      b ^= 1;
+    }
+    const int blocks = (int)((M + (OT / 32) - 1) / (OT / 32)) < sms * 4
+                           ? (int)((M + (OT / 32) - 1) / (OT / 32))
+                           : sms * 4;
+    k_out_rank<<<blocks, OT, osmem, st>>>(in, ldin, net->d_w + ho.w_off, ho.pitch, M, ho.fi,
+                                          ho.fo, out ? out + m0 * ho.fo : nullptr,
+                                          labels ? labels + m0 : nullptr,
+                                          reinterpret_cast<unsigned long long*>(counts),
+                                          guess ? guess + 2 * m0 : nullptr);
+    if (int rc = cuda_check(cudaGetLastError(), "eval kernels")) return rc;
+  }
+  return DMLP_OK;
+}
+
+}  // namespace dmlp
+
+using namespace dmlp;
+
+extern "C" {
+
+int dmlp_forward_batch(dmlp_net* net, const float* x_dev, int64_t n, float* out_dev,
+                       void* stream) {
+  if (!net) return set_error(DMLP_EINVAL, "null net");
+  if (n > 0 && (!x_dev || !out_dev)) return set_error(DMLP_EINVAL, "null argument");
+  return run_eval(net, x_dev, n, out_dev, nullptr, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int dmlp_eval_counts(dmlp_net* net, const float* x_dev, const uint8_t* labels_dev, int64_t n,
+                     int64_t* counts_dev, int32_t* guess_dev, void* stream) {
+  if (!net) return set_error(DMLP_EINVAL, "null net");
+  if (n > 0 && (!x_dev || !labels_dev || !counts_dev))
+    return set_error(DMLP_EINVAL, "null argument");
+  return run_eval(net, x_dev, n, nullptr, labels_dev, (long long*)counts_dev, guess_dev,
+                  (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+"""DeviceNet: the device-resident network state behind the C-ABI.
+
+Owns one `dmlp_net` (include/dmlp.h).  Device buffers passed in and out are
+torch CUDA tensors (PyTorch is the plumbing: allocation, streams,
+torch.distributed); all arithmetic runs in libdmlp's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import SizeMismatch
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1003_0358_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def current_stream_handle(device: int = 0) -> ctypes.c_void_p:
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class DeviceNet:
+    """Padded, device-resident copy of an Mlp plus the persistent-kernel state."""
+
+    def __init__(self, layer_sizes, device: int = 0, residency: str = "auto", n_ctas: int = 0):
+        _torch()
+        self.layer_sizes = tuple(int(s) for s in layer_sizes)
+        self.device = int(device)
+        sizes = (ctypes.c_int32 * len(self.layer_sizes))(*self.layer_sizes)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().dmlp_net_create(self.device, sizes, len(self.layer_sizes),
+                                              _lib.RESIDENCY[residency], int(n_ctas),
+                                              ctypes.byref(h)), "dmlp_net_create")
+        self._h = h
+        r, c, t, s = (ctypes.c_int32() for _ in range(4))
+        _lib.check(_lib.lib().dmlp_net_info(self._h, ctypes.byref(r), ctypes.byref(c),
+                                            ctypes.byref(t), ctypes.byref(s)), "dmlp_net_info")
+        self.residency = {v: k for k, v in _lib.RESIDENCY.items()}[r.value]
+        self.n_ctas, self.threads, self.smem_bytes = c.value, t.value, s.value
+
+    # -- lifetime ---------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().dmlp_net_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def shapes(self):
+        s = self.layer_sizes
+        return [(o, i + 1) for i, o in zip(s[:-1], s[1:])]
+
+    # -- weights (K5 pack / unpack) ---------------------------------------------
+    def set_layers(self, layers) -> None:
+        if len(layers) != len(self.shapes):
+            raise SizeMismatch(f"{len(layers)} layers for a {len(self.shapes)}-layer net")
+        for li, (w, shape) in enumerate(zip(layers, self.shapes)):
+            if tuple(w.shape) != shape:
+                raise SizeMismatch(f"layer {li} shape {tuple(w.shape)}, want {shape}")
+            if isinstance(w, np.ndarray):
+                w = np.ascontiguousarray(w, dtype=np.float32)
+                p = w.ctypes.data_as(ctypes.c_void_p)
+            else:  # torch tensor (host or device)
+                w = w.contiguous().float()
+                p = _ptr(w)
+            _lib.check(_lib.lib().dmlp_net_set_layer(self._h, li, p, w.size if isinstance(
+                w, np.ndarray) else w.numel()), "dmlp_net_set_layer")
+
+    def get_layers(self) -> list[np.ndarray]:
+        out = []
+        for li, shape in enumerate(self.shapes):
+            w = np.empty(shape, dtype=np.float32)
+            _lib.check(_lib.lib().dmlp_net_get_layer(self._h, li, w.ctypes.data_as(ctypes.c_void_p),
+                                                     w.size), "dmlp_net_get_layer")
+            out.append(w)
+        return out
+
+    # -- in-kernel profile ----------------------------------------------------------
+    def profile(self, enable: bool = True) -> None:
+        _lib.check(_lib.lib().dmlp_net_profile(self._h, int(bool(enable))), "dmlp_net_profile")
+
+    def read_profile(self) -> dict:
+        """Sums over CTAs since the last read: sample-loop cycles and cycles
+        spent waiting in inter-CTA exchanges ("grid-sync stall")."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().dmlp_net_read_profile(self._h, ctypes.byref(a), ctypes.byref(b)),
+                   "dmlp_net_read_profile")
+        return {"loop_cycles": a.value, "exchange_cycles": b.value,
+                "exchange_fraction": (b.value / a.value) if a.value else 0.0}
+
+    # -- training -----------------------------------------------------------------
+    def train_step(self, x: np.ndarray, digit: int, eta: float) -> np.ndarray:
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float32).ravel())
+        if x.shape[0] != self.layer_sizes[0]:
+            raise SizeMismatch(f"input length {x.shape[0]}, layer fan_in {self.layer_sizes[0]}")
+        if eta < 0:
+            raise ValueError("eta must be non-negative")
+        y = np.empty(self.layer_sizes[-1], dtype=np.float32)
+        _lib.check(_lib.lib().dmlp_train_step(self._h, x.ctypes.data_as(ctypes.c_void_p),
+                                              int(digit), float(np.float32(eta)),
+                                              y.ctypes.data_as(ctypes.c_void_p)),
+                   "dmlp_train_step")
+        return y
+
+    def train_epoch(self, x, labels, order, eta: float, wrong, y_last=None, stream=None) -> None:
+        """Asynchronous on `stream` (default: torch's current stream).
+
+        x: (n, >=fan_in) f32 CUDA tensor; labels: (n,) u8; order: (n,) i32 or
+        None; wrong: int64 CUDA scalar accumulating argmax errors."""
+        if eta < 0:
+            raise ValueError("eta must be non-negative")
+        n = int(order.numel()) if order is not None else int(x.shape[0])
+        ldx = int(x.stride(0))
+        st = stream if stream is not None else current_stream_handle(self.device)
+        _lib.check(_lib.lib().dmlp_train_epoch(self._h, _ptr(x), ldx, _ptr(labels), _ptr(order),
+                                               n, float(np.float32(eta)), _ptr(wrong),
+                                               _ptr(y_last), st), "dmlp_train_epoch")
+
+    # -- evaluation ---------------------------------------------------------------
+    def forward_batch(self, x, out=None, stream=None):
+        torch = _torch()
+        n = int(x.shape[0])
+        if x.dim() != 2 or x.shape[1] != self.layer_sizes[0] or not x.is_contiguous():
+            raise SizeMismatch(f"batch shape {tuple(x.shape)}, want (n, {self.layer_sizes[0]})")
+        if out is None:
+            out = torch.empty((n, self.layer_sizes[-1]), dtype=torch.float32, device=x.device)
+        st = stream if stream is not None else current_stream_handle(self.device)
+        _lib.check(_lib.lib().dmlp_forward_batch(self._h, _ptr(x), n, _ptr(out), st),
+                   "dmlp_forward_batch")
+        return out
+
+    def eval_counts(self, x, labels, counts=None, guess=None, stream=None):
+        """counts (int64[102]) += {wrong, confusion[10][10], second_correct}."""
+        torch = _torch()
+        n = int(x.shape[0])
+        if x.dim() != 2 or x.shape[1] != self.layer_sizes[0] or not x.is_contiguous():
+            raise SizeMismatch(f"batch shape {tuple(x.shape)}, want (n, {self.layer_sizes[0]})")
+        if counts is None:
+            counts = torch.zeros(102, dtype=torch.int64, device=x.device)
+        st = stream if stream is not None else current_stream_handle(self.device)
+        _lib.check(_lib.lib().dmlp_eval_counts(self._h, _ptr(x), _ptr(labels), n, _ptr(counts),
+                                               _ptr(guess), st), "dmlp_eval_counts")
+        return counts

@@ -1,0 +1,146 @@
+"""GPU parity: persistent training kernel vs the CPU oracle (bit-pinned to the
+reference).  Tolerances (north star):
+  * per step: identical argmax, outputs within 2e-5 absolute;
+  * after K steps, per layer: max|W_gpu - W_ref| <= 1e-5 * max|W_ref| and
+    ||W_gpu - W_ref||_2 <= 1e-5 * ||W_ref||_2.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+W_TOL = 1e-5
+
+
+def _net(sizes, layers, **kw):
+    from paper_1003_0358_b200.device import DeviceNet
+
+    dn = DeviceNet(sizes, **kw)
+    dn.set_layers(layers)
+    return dn
+
+
+def _assert_weights_close(got, ref, tol=W_TOL):
+    for li, (g, r) in enumerate(zip(got, ref)):
+        d = np.abs(g.astype(np.float64) - r)
+        assert d.max() <= tol * np.abs(r).max(), (li, d.max(), np.abs(r).max())
+        assert np.linalg.norm(d) <= tol * np.linalg.norm(r), (li, np.linalg.norm(d))
+
+
+def _inputs(golden):
+    g = golden("train")
+    return g["deformed"].reshape(64, -1), g["labels"]
+
+
+def test_pack_unpack_roundtrip():
+    sizes = (841, 70, 33, 10)
+    layers = O.init_layers(3, sizes)
+    dn = _net(sizes, layers)
+    for a, b in zip(dn.get_layers(), layers):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("residency", ["l2", "smem"])
+def test_train_step_small_vs_golden(golden, residency):
+    g = golden("train")
+    x, lab = _inputs(golden)
+    sizes = (841, 70, 33, 10)
+    layers = O.init_layers(0, sizes)
+    dn = _net(sizes, layers, residency=residency, n_ctas=8)
+    for s in range(40):
+        i = s % 64
+        y = dn.train_step(x[i], int(lab[i]), 1e-3)
+        yref = g["small_outputs"][s]
+        assert np.argmax(y) == np.argmax(yref)
+        assert np.abs(y - yref).max() < 2e-5, (s, np.abs(y - yref).max())
+    ref = []
+    pos = 0
+    for shp in O.layer_shapes(sizes):
+        ref.append(g["small_final"][pos:pos + shp[0] * shp[1]].reshape(shp))
+        pos += shp[0] * shp[1]
+    _assert_weights_close(dn.get_layers(), ref)
+
+
+def test_train_step_c1_1000_steps(golden):
+    """North-star check: 1000 on-line steps with identical (injected) inputs."""
+    x, lab = _inputs(golden)
+    sizes = (841, 1000, 500, 10)
+    ref = O.init_layers(0, sizes)
+    dn = _net(sizes, [w.copy() for w in ref])
+    O.set_threads(8)
+    rng = np.random.default_rng(1)
+    for s in range(1000):
+        i = int(rng.integers(64))
+        y = dn.train_step(x[i], int(lab[i]), 1e-3)
+        yr = O.train_step(ref, x[i], int(lab[i]), 1e-3)
+        assert np.argmax(y) == np.argmax(yr), s
+    _assert_weights_close(dn.get_layers(), ref)
+
+
+@pytest.mark.parametrize("n_ctas", [0, 7, 32])
+def test_train_epoch_matches_steps(golden, n_ctas):
+    """One persistent launch over a shuffled order == the oracle's epoch."""
+    import torch
+
+    g = golden("train")
+    x, lab = _inputs(golden)
+    sizes = (841, 70, 33, 10)
+    ref = O.init_layers(0, sizes)
+    dn = _net(sizes, [w.copy() for w in ref], n_ctas=n_ctas)
+    perm = O.substream(0, 3, 0).permutation(64)
+    wrong_ref = O.train_epoch(ref, g["deformed"], lab, 1e-3, order=perm)
+    xd = torch.from_numpy(x).cuda()
+    ld = torch.from_numpy(lab).cuda()
+    od = torch.from_numpy(perm.astype(np.int32)).cuda()
+    wrong = torch.zeros((), dtype=torch.int64, device="cuda")
+    dn.train_epoch(xd, ld, od, 1e-3, wrong)
+    torch.cuda.synchronize()
+    assert int(wrong.item()) == wrong_ref
+    _assert_weights_close(dn.get_layers(), ref)
+
+
+def test_train_epoch_deterministic(golden):
+    import torch
+
+    x, lab = _inputs(golden)
+    sizes = (841, 300, 120, 10)
+    base = O.init_layers(7, sizes)
+    outs = []
+    for _ in range(2):
+        dn = _net(sizes, [w.copy() for w in base])
+        wrong = torch.zeros((), dtype=torch.int64, device="cuda")
+        xd = torch.from_numpy(np.tile(x, (4, 1))).cuda()
+        ld = torch.from_numpy(np.tile(lab, 4)).cuda()
+        dn.train_epoch(xd, ld, None, 1e-3, wrong)
+        outs.append(np.concatenate([w.ravel() for w in dn.get_layers()]))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_deep_net_c5_shape(golden):
+    """C5-like depth (9 hidden layers) at reduced width: many exchange hops."""
+    x, lab = _inputs(golden)
+    sizes = (841,) + (160,) * 9 + (10,)
+    ref = O.init_layers(2, sizes)
+    dn = _net(sizes, [w.copy() for w in ref])
+    for s in range(50):
+        y = dn.train_step(x[s], int(lab[s]), 1e-3)
+        yr = O.train_step(ref, x[s], int(lab[s]), 1e-3)
+        assert np.argmax(y) == np.argmax(yr)
+        assert np.abs(y - yr).max() < 2e-5
+    _assert_weights_close(dn.get_layers(), ref)
+
+
+def test_errors_map_to_reference_exceptions():
+    from paper_1003_0358_b200.device import DeviceNet
+    from paper_1003_0358_b200.errors import SizeMismatch
+
+    dn = DeviceNet((841, 20, 10))
+    with pytest.raises(SizeMismatch):
+        dn.set_layers([np.zeros((20, 841), np.float32), np.zeros((10, 21), np.float32)])
+    with pytest.raises(SizeMismatch):
+        dn.train_step(np.zeros(840, np.float32), 1, 1e-3)
+    with pytest.raises(ValueError):
+        dn.train_step(np.zeros(841, np.float32), 1, -1.0)
