@@ -30,9 +30,11 @@ extern "C" {
 #define DMLP_ENCCL 4
 
 /* Weight residency of the persistent training kernel. */
-#define DMLP_RES_AUTO 0   /* smem-resident when the net fits on chip, else L2-streamed */
+#define DMLP_RES_AUTO 0   /* keep the largest set of layers that fits in smem, stream the rest */
 #define DMLP_RES_L2 1     /* weights in HBM, L2-persisting window, streamed every sample */
 #define DMLP_RES_SMEM 2   /* every CTA keeps its owned rows in shared memory */
+#define DMLP_RES_HYBRID 3 /* (reported only) some layers resident, the rest streamed */
+#define DMLP_RES_MASK 0x10000 /* DMLP_RES_MASK | m: exactly the layers in bitmask m resident */
 
 typedef struct dmlp_net dmlp_net;
 
@@ -69,11 +71,17 @@ int dmlp_net_set_layer(dmlp_net *net, int32_t layer, const float *w, int64_t n);
 /* Unpack one layer back into the reference layout (host or device pointer). */
 int dmlp_net_get_layer(dmlp_net *net, int32_t layer, float *w, int64_t n);
 
-/* In-kernel profile of the persistent training kernel: when enabled, every
- * CTA accumulates the cycles of its sample loop and the cycles spent in the
- * inter-CTA exchange waits.  read returns the sums over CTAs and resets. */
+/* In-kernel profile of the persistent training kernel: when enabled, thread
+ * 0 of every CTA accumulates per-phase cycle counts.  read fills slots[16]
+ * with the sums over CTAs and resets them: slot 0 = sample-loop cycles,
+ * 1 = cycles waiting in inter-CTA exchanges, 2.. = phases. */
 int dmlp_net_profile(dmlp_net *net, int32_t enable);
-int dmlp_net_read_profile(dmlp_net *net, int64_t *loop_cycles, int64_t *exchange_cycles);
+int dmlp_net_read_profile(dmlp_net *net, int64_t *slots);
+/* One-sample timeline of the next launches: every CTA records %globaltimer
+ * at 64 marks of sample `sample` (mark 0 start; for exchange e, 1+2e = its
+ * contribution published, 2+2e = its gather done; 63 end).  marks (optional,
+ * [n_ctas][64]) receives the previous recording; sample < 0 disables. */
+int dmlp_net_trace(dmlp_net *net, int64_t sample, uint64_t *marks);
 
 /* ---- on-line training (kernels.train_step / trainer.train_epoch) ---- */
 
@@ -123,6 +131,19 @@ int dmlp_deform_injected(const uint8_t *raw_dev, int64_t n, const double *noise_
 
 /* deform.upscale_dataset (deform.py:250-257): (n,28,28) u8 -> (n,841) f32. */
 int dmlp_upscale(const uint8_t *raw_dev, int64_t n, float *out_dev, void *stream);
+
+/* ---- K6 microbenchmarks (roofline denominators, exchange floor) ----
+ * kind 0: streaming read of `bytes` (float4, .cg), `iters` passes;
+ * kind 1: streaming read+write; kind 2: shared-memory read+write, 128 KB
+ * per CTA, `iters` passes; kind 3: exchange ping, `iters` rounds.
+ * One 512-thread CTA per SM unless n_ctas > 0.  Returns wall seconds
+ * (CUDA events) and the slowest CTA's clock64 cycles. */
+int dmlp_bench(int32_t kind, int64_t bytes, int32_t iters, int32_t n_ctas, double *seconds,
+               double *cycles);
+/* Cycles per op of the sample loop's primitives: [0] __syncthreads (512
+ * threads), [1] exact scaled tanh, [2] IEEE fp32 divide, [3] warp shuffle
+ * reduction, [4] dependent L2 load, [5] dependent ld.relaxed.gpu, [6] smem load. */
+int dmlp_bench_prims(double *out);
 
 #ifdef __cplusplus
 }

@@ -15,8 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdmlp.so")
 
 DMLP_OK, DMLP_ESIZE, DMLP_EINVAL, DMLP_ECUDA, DMLP_ENCCL = 0, 1, 2, 3, 4
-RES_AUTO, RES_L2, RES_SMEM = 0, 1, 2
-RESIDENCY = {"auto": RES_AUTO, "l2": RES_L2, "smem": RES_SMEM}
+RES_AUTO, RES_L2, RES_SMEM, RES_HYBRID = 0, 1, 2, 3
+RESIDENCY = {"auto": RES_AUTO, "l2": RES_L2, "smem": RES_SMEM, "hybrid": RES_HYBRID}
 
 # (function name, restype, argtypes) -- must match include/dmlp.h exactly.
 P, i32, i64, u64, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
@@ -40,7 +40,8 @@ SIGNATURES = [
     ("dmlp_net_destroy", ctypes.c_int, [P]),
     ("dmlp_net_info", ctypes.c_int, [P, I32P, I32P, I32P, I32P]),
     ("dmlp_net_profile", ctypes.c_int, [P, i32]),
-    ("dmlp_net_read_profile", ctypes.c_int, [P, I64P, I64P]),
+    ("dmlp_net_read_profile", ctypes.c_int, [P, I64P]),
+    ("dmlp_net_trace", ctypes.c_int, [P, i64, P]),
     ("dmlp_net_set_layer", ctypes.c_int, [P, i32, P, i64]),
     ("dmlp_net_get_layer", ctypes.c_int, [P, i32, P, i64]),
     ("dmlp_train_step", ctypes.c_int, [P, P, i32, f32, P]),
@@ -50,6 +51,9 @@ SIGNATURES = [
     ("dmlp_deform", ctypes.c_int, [P, P, i64, i64, u64, u64, ctypes.POINTER(DeformParamsC), P, P]),
     ("dmlp_deform_injected", ctypes.c_int, [P, i64, P, P, P, i32, P, P]),
     ("dmlp_upscale", ctypes.c_int, [P, i64, P, P]),
+    ("dmlp_bench", ctypes.c_int, [i32, i64, i32, i32, ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double)]),
+    ("dmlp_bench_prims", ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
 ]
 
 _lib = None

@@ -27,6 +27,7 @@ UNITS = {
     "train_kernel.cu": [],
     "eval_kernel.cu": [],
     "deform_kernel.cu": ["-fmad=false"],
+    "microbench.cu": [],
 }
 
 

@@ -32,6 +32,16 @@ int cuda_check(cudaError_t e, const char* what) {
   return set_error(DMLP_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
+// Every operation on a net waits for the previous one (whatever stream it ran
+// on) and records net->done when it is enqueued: weights are never read or
+// written concurrently by two streams.
+int net_begin(dmlp_net* net, cudaStream_t st) {
+  return cuda_check(cudaStreamWaitEvent(st, net->done, 0), "cudaStreamWaitEvent");
+}
+int net_end(dmlp_net* net, cudaStream_t st) {
+  return cuda_check(cudaEventRecord(net->done, st), "cudaEventRecord");
+}
+
 #define DMLP_CUDA(call)                                 \
   do {                                                  \
     int _rc = ::dmlp::cuda_check((call), #call);        \
@@ -64,17 +74,16 @@ __global__ void k_unpack(const float* __restrict__ src, float* __restrict__ dst,
   }
 }
 
-static int own_max_rows(int fo, int nct) {
-  int m = 0;
-  for (int c = 0; c < nct; c++) {
-    const int r0 = (int)((long long)fo * c / nct), r1 = (int)((long long)fo * (c + 1) / nct);
-    if (r1 - r0 > m) m = r1 - r0;
-  }
-  return m;
+// Rows per CTA block: CTA c owns rows [c*R, min(c*R + R, fo)).
+static int own_max_rows(int fo, int nct) { return (fo + nct - 1) / nct; }
+static int ceil_log2(int x) {
+  int l = 0;
+  while ((1 << l) < x) l++;
+  return l;
 }
 
-// Lay out dynamic shared memory; returns bytes.
-static int layout_smem(dmlp_net* net, bool resident) {
+// Lay out dynamic shared memory for a resident-layer mask; returns bytes.
+static int layout_smem(dmlp_net* net, unsigned mask) {
   NetDev& d = net->dev;
   const int L = d.L;
   int off = 0;
@@ -99,17 +108,34 @@ static int layout_smem(dmlp_net* net, bool resident) {
     d.dsc_off[b] = take(maxr);
   }
   d.red_off = take(kWarps * 32);
+  d.pbuf_off = take(4 * kThreads);
+  int xb = 1;
+  for (int l = 1; l < L - 1; l++) {
+    const int need = d.ly[l].P * d.ly[l - 1].R;
+    if (need > xb) xb = need;
+  }
+  d.xbuf_off = take(xb);
   d.out_off = take(4 * kMaxOut);
-  d.wsm_off = off;
-  if (resident) {
-    int w = 0;
-    for (int l = 0; l < L; l++) {
+  for (int l = 0; l < L; l++) {
+    d.ly[l].res = (mask >> l) & 1u;
+    d.ly[l].wsm_off = 0;
+    if (d.ly[l].res) {
       const int r = (l < L - 1) ? own_max_rows(d.ly[l].fo, d.nct) : d.ly[l].fo;
-      w += r * d.ly[l].pitch;
+      d.ly[l].wsm_off = take(r * d.ly[l].pitch);
     }
-    take(w);
   }
   return off * (int)sizeof(float);
+}
+
+// Resident-layer mask for a residency policy: all, none, or (AUTO) the subset
+// that keeps the most weight bytes on chip within the smem budget.
+static long long resident_floats(const NetDev& d, unsigned mask) {
+  long long f = 0;
+  for (int l = 0; l < d.L; l++)
+    if ((mask >> l) & 1u)
+      f += (long long)((l < d.L - 1) ? own_max_rows(d.ly[l].fo, d.nct) : d.ly[l].fo) *
+           d.ly[l].pitch;
+  return f;
 }
 
 }  // namespace dmlp
@@ -143,7 +169,7 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     if (sizes[i] < 1) return set_error(DMLP_EINVAL, "layer sizes must be positive");
   if (sizes[n_sizes - 1] > kMaxOut)
     return set_error(DMLP_EINVAL, "output layer wider than %d is not supported", kMaxOut);
-  if (residency < DMLP_RES_AUTO || residency > DMLP_RES_SMEM)
+  if ((residency < DMLP_RES_AUTO || residency > DMLP_RES_SMEM) && !(residency & DMLP_RES_MASK))
     return set_error(DMLP_EINVAL, "unknown residency %d", residency);
   DMLP_CUDA(cudaSetDevice(device));
   cudaDeviceProp prop;
@@ -160,8 +186,6 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
   d.L = n_sizes - 1;
   int nct = n_ctas > 0 ? n_ctas : prop.multiProcessorCount;
   if (nct > prop.multiProcessorCount) nct = prop.multiProcessorCount;
-  for (int l = 0; l < d.L; l++)  // every CTA must own at least one row of every hidden layer
-    if (l < d.L - 1 && sizes[l + 1] < nct) nct = sizes[l + 1];
   d.nct = nct;
 
   size_t woff = 0;
@@ -179,39 +203,68 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
   }
   net->w_floats = woff;
 
-  // exchange buffers: y words [2][fo] for hidden layers, partial words [2][nct][pitch] for l>=1
+  // exchange buffers (line-aligned per producer): y words [2][P][1<<ylog] for
+  // hidden layers, partial words [2][P][pstride] for hidden layers l >= 1
   size_t ll = 0;
   size_t yoff[kMaxLayers], poff[kMaxLayers];
   for (int l = 0; l < d.L - 1; l++) {
+    LayerDev& ly = d.ly[l];
+    ly.R = own_max_rows(ly.fo, nct);
+    if (ly.R > 4 * kThreads) {
+      delete net;
+      return set_error(DMLP_EINVAL, "layer %d: %d rows per CTA exceed the staging buffer", l,
+                       ly.R);
+    }
+    ly.P = (ly.fo + ly.R - 1) / ly.R;
+    ly.ylog = ceil_log2(ly.R < 16 ? 16 : ly.R);
+    ly.pstride = round_up(ly.fi, 16);
     yoff[l] = ll;
-    ll += 2 * (size_t)d.ly[l].fo;
+    ll += 2 * (size_t)ly.P << ly.ylog;
     if (l >= 1) {
       poff[l] = ll;
-      ll += 2 * (size_t)nct * d.ly[l].pitch;
+      ll += 2 * (size_t)ly.P * ly.pstride;
     }
   }
   net->ll_words = ll;
 
-  // residency
-  int smem_l2 = layout_smem(net, false);
-  int smem_res = layout_smem(net, true);
-  const int smem_cap = (int)prop.sharedMemPerBlockOptin;
-  int res = residency;
-  if (res == DMLP_RES_AUTO) res = (smem_res <= smem_cap) ? DMLP_RES_SMEM : DMLP_RES_L2;
-  if (res == DMLP_RES_SMEM && smem_res > smem_cap) {
-    delete net;
-    return set_error(DMLP_EINVAL,
-                     "net does not fit in shared memory: %d bytes per CTA needed, %d available",
-                     smem_res, smem_cap);
+  // residency: choose which layers keep their rows in shared memory
+  const int smem_cap = (int)prop.sharedMemPerBlockOptin - 1024;  // keep room for static smem
+  const unsigned all = (d.L >= 32) ? 0xFFFFFFFFu : ((1u << d.L) - 1u);
+  unsigned mask = 0;
+  if (residency & DMLP_RES_MASK) {
+    mask = (unsigned)residency & all;
+    if (layout_smem(net, mask) > smem_cap) {
+      const int need = layout_smem(net, mask);
+      delete net;
+      return set_error(DMLP_EINVAL, "resident-layer mask needs %d bytes of smem (> %d)", need,
+                       smem_cap);
+    }
+  } else if (residency == DMLP_RES_SMEM) {
+    mask = all;
+    if (layout_smem(net, mask) > smem_cap) {
+      const int need = layout_smem(net, mask);
+      delete net;
+      return set_error(DMLP_EINVAL,
+                       "net does not fit in shared memory: %d bytes per CTA needed, %d available",
+                       need, smem_cap);
+    }
+  } else if (residency == DMLP_RES_AUTO) {
+    long long best = -1;
+    for (unsigned m = 0; m <= all; m++) {
+      if (layout_smem(net, m) > smem_cap) continue;
+      const long long f = resident_floats(d, m);
+      if (f > best) { best = f; mask = m; }
+    }
   }
-  if (smem_l2 > smem_cap) {
+  if (layout_smem(net, 0) > smem_cap) {
+    const int need = layout_smem(net, 0);
     delete net;
     return set_error(DMLP_EINVAL, "activation vectors need %d bytes of shared memory (> %d)",
-                     smem_l2, smem_cap);
+                     need, smem_cap);
   }
-  net->residency = res;
-  d.resident = (res == DMLP_RES_SMEM) ? 1 : 0;
-  net->smem_bytes = layout_smem(net, d.resident != 0);
+  net->residency = mask == all ? DMLP_RES_SMEM : (mask == 0 ? DMLP_RES_L2 : DMLP_RES_HYBRID);
+  net->smem_bytes = layout_smem(net, mask);
+  net->resident_mask = mask;
 
   int rc = DMLP_OK;
   auto fail = [&](int code) {
@@ -241,6 +294,9 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     return fail(rc);
   if ((rc = cuda_check(cudaMalloc(&net->d_stage_lab, 64), "cudaMalloc"))) return fail(rc);
   if ((rc = cuda_check(cudaMalloc(&net->d_stage_wrong, 64), "cudaMalloc"))) return fail(rc);
+  if ((rc = cuda_check(cudaEventCreateWithFlags(&net->done, cudaEventDisableTiming),
+                       "cudaEventCreate")))
+    return fail(rc);
   if ((rc = cuda_check(cudaStreamCreateWithFlags(&net->stream, cudaStreamNonBlocking),
                        "cudaStreamCreate")))
     return fail(rc);
@@ -251,6 +307,8 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
   }
   d.err = net->d_err;
   d.prof = nullptr;
+  d.trace = nullptr;
+  d.trace_sample = -1;
   *out = net;
   return DMLP_OK;
 }
@@ -258,7 +316,7 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
 int dmlp_net_destroy(dmlp_net* net) {
   if (!net) return DMLP_OK;
   cudaSetDevice(net->device);
-  if (net->stream) cudaStreamSynchronize(net->stream);
+  cudaDeviceSynchronize();
   cudaFree(net->d_w);
   cudaFree(net->d_ll);
   cudaFree(net->d_err);
@@ -268,7 +326,9 @@ int dmlp_net_destroy(dmlp_net* net) {
   cudaFree(net->d_act[0]);
   cudaFree(net->d_act[1]);
   cudaFree(net->dev.prof);
+  cudaFree(net->dev.trace);
   if (net->stream) cudaStreamDestroy(net->stream);
+  if (net->done) cudaEventDestroy(net->done);
   delete net;
   return DMLP_OK;
 }
@@ -289,23 +349,43 @@ int dmlp_net_profile(dmlp_net* net, int32_t enable) {
   DMLP_CUDA(cudaStreamSynchronize(net->stream));
   if (enable && !net->dev.prof) {
     unsigned long long* p = nullptr;
-    DMLP_CUDA(cudaMalloc(&p, 2 * sizeof(unsigned long long) * net->dev.nct));
-    DMLP_CUDA(cudaMemset(p, 0, 2 * sizeof(unsigned long long) * net->dev.nct));
+    DMLP_CUDA(cudaMalloc(&p, kProfWords * sizeof(unsigned long long) * net->dev.nct));
+    DMLP_CUDA(cudaMemset(p, 0, kProfWords * sizeof(unsigned long long) * net->dev.nct));
     net->dev.prof = p;
   } else if (!enable && net->dev.prof) {
     DMLP_CUDA(cudaDeviceSynchronize());
     cudaFree(net->dev.prof);
+  cudaFree(net->dev.trace);
     net->dev.prof = nullptr;
   }
   return DMLP_OK;
 }
 
-int dmlp_net_read_profile(dmlp_net* net, int64_t* loop_cycles, int64_t* exchange_cycles) {
+int dmlp_net_trace(dmlp_net* net, int64_t sample, uint64_t* marks /* [n_ctas][64] or NULL */) {
   if (!net) return set_error(DMLP_EINVAL, "null net");
+  DMLP_CUDA(cudaSetDevice(net->device));
+  DMLP_CUDA(cudaDeviceSynchronize());
+  const size_t bytes = (size_t)net->dev.nct * 64 * sizeof(unsigned long long);
+  if (marks && net->dev.trace) {  // read back the previous launch's marks
+    DMLP_CUDA(cudaMemcpy(marks, net->dev.trace, bytes, cudaMemcpyDeviceToHost));
+  }
+  if (sample >= 0) {
+    if (!net->dev.trace) DMLP_CUDA(cudaMalloc(&net->dev.trace, bytes));
+    DMLP_CUDA(cudaMemset(net->dev.trace, 0, bytes));
+    net->dev.trace_sample = sample;
+  } else if (net->dev.trace) {
+    cudaFree(net->dev.trace);
+    net->dev.trace = nullptr;
+  }
+  return DMLP_OK;
+}
+
+int dmlp_net_read_profile(dmlp_net* net, int64_t* slots) {
+  if (!net || !slots) return set_error(DMLP_EINVAL, "null argument");
   if (!net->dev.prof) return set_error(DMLP_EINVAL, "profiling is not enabled");
   DMLP_CUDA(cudaSetDevice(net->device));
   DMLP_CUDA(cudaDeviceSynchronize());
-  const int n = 2 * net->dev.nct;
+  const int n = kProfWords * net->dev.nct;
   unsigned long long* h = new unsigned long long[n];
   cudaError_t e = cudaMemcpy(h, net->dev.prof, n * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost);
@@ -313,14 +393,12 @@ int dmlp_net_read_profile(dmlp_net* net, int64_t* loop_cycles, int64_t* exchange
     delete[] h;
     return cuda_check(e, "cudaMemcpy profile");
   }
-  long long a = 0, b = 0;
-  for (int c = 0; c < net->dev.nct; c++) {
-    a += (long long)h[2 * c];
-    b += (long long)h[2 * c + 1];
+  for (int k = 0; k < kProfWords; k++) {
+    long long a = 0;
+    for (int c = 0; c < net->dev.nct; c++) a += (long long)h[kProfWords * c + k];
+    slots[k] = a;
   }
   delete[] h;
-  if (loop_cycles) *loop_cycles = a;
-  if (exchange_cycles) *exchange_cycles = b;
   DMLP_CUDA(cudaMemset(net->dev.prof, 0, n * sizeof(unsigned long long)));
   return DMLP_OK;
 }
@@ -334,12 +412,14 @@ int dmlp_net_set_layer(dmlp_net* net, int32_t layer, const float* w, int64_t n) 
                      (long long)h.fo * (h.fi + 1), (long long)n);
   DMLP_CUDA(cudaSetDevice(net->device));
   float* tmp = nullptr;
+  DMLP_CUDA(cudaStreamWaitEvent(net->stream, net->done, 0));
   DMLP_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), net->stream));
   DMLP_CUDA(cudaMemcpyAsync(tmp, w, n * sizeof(float), cudaMemcpyDefault, net->stream));
   k_pack<<<296, 256, 0, net->stream>>>(tmp, net->d_w + h.w_off, h.fo, h.fi, h.pitch,
                                        (int)h.copies);
   DMLP_CUDA(cudaGetLastError());
   DMLP_CUDA(cudaFreeAsync(tmp, net->stream));
+  DMLP_CUDA(cudaEventRecord(net->done, net->stream));
   DMLP_CUDA(cudaStreamSynchronize(net->stream));
   return DMLP_OK;
 }
@@ -353,11 +433,13 @@ int dmlp_net_get_layer(dmlp_net* net, int32_t layer, float* w, int64_t n) {
                      (long long)h.fo * (h.fi + 1), (long long)n);
   DMLP_CUDA(cudaSetDevice(net->device));
   float* tmp = nullptr;
+  DMLP_CUDA(cudaStreamWaitEvent(net->stream, net->done, 0));
   DMLP_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), net->stream));
   k_unpack<<<296, 256, 0, net->stream>>>(net->d_w + h.w_off, tmp, h.fo, h.fi, h.pitch);
   DMLP_CUDA(cudaGetLastError());
   DMLP_CUDA(cudaMemcpyAsync(w, tmp, n * sizeof(float), cudaMemcpyDefault, net->stream));
   DMLP_CUDA(cudaFreeAsync(tmp, net->stream));
+  DMLP_CUDA(cudaEventRecord(net->done, net->stream));
   DMLP_CUDA(cudaStreamSynchronize(net->stream));
   return DMLP_OK;
 }
@@ -387,8 +469,10 @@ static int run_epoch(dmlp_net* net, const float* x, long long ldx, const uint8_t
     net->seq = 1;
   }
   const uint32_t seq0 = net->seq;
+  if (int rc = net_begin(net, st)) return rc;
   cudaError_t e = launch_train(net, x, ldx, labels, order, n, eta, seq0, wrong, y_last, st);
   if (e != cudaSuccess) return check_kernel_error(net, e);
+  if (int rc = net_end(net, st)) return rc;
   net->seq += (uint32_t)n;
   return DMLP_OK;
 }
@@ -400,6 +484,7 @@ int dmlp_train_step(dmlp_net* net, const float* x, int32_t digit, float eta, flo
   DMLP_CUDA(cudaSetDevice(net->device));
   const int fi0 = net->sizes[0];
   uint8_t lab = (uint8_t)digit;
+  DMLP_CUDA(cudaStreamWaitEvent(net->stream, net->done, 0));
   DMLP_CUDA(cudaMemcpyAsync(net->d_stage, x, fi0 * sizeof(float), cudaMemcpyDefault, net->stream));
   DMLP_CUDA(cudaMemcpyAsync(net->d_stage_lab, &lab, 1, cudaMemcpyHostToDevice, net->stream));
   float* ydev = net->d_stage + round_up(fi0, 32);

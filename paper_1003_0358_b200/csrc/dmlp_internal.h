@@ -13,29 +13,40 @@ constexpr int kThreads = 512;  // threads per CTA of the persistent kernel
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLayers = 16;
 constexpr int kMaxOut = 32;  // replicated output layer: at most 32 classes
+constexpr int kProfWords = 16;  // profile slots per CTA
 
 // One weight layer as the persistent kernel sees it.
 struct LayerDev {
   int fi, fo, pitch;     // fan-in, fan-out, floats per device row (>= fi+1, %4 == 0)
   int in_off;            // smem offset (floats) of this layer's input vector (pitch long)
   int t_off;             // smem offset of the owned rows' tanh(B*a) cache
+  int res;               // 1: the CTA's rows of this layer live in shared memory
+  int wsm_off;           // resident: smem offset of the owned rows (or the output copy)
+  int R;                 // hidden: rows per CTA block; CTA c owns [c*R, min(c*R+R, fo))
+  int P;                 // hidden: CTAs owning at least one row = ceil(fo / R)
+  int ylog;              // hidden: log2 of the per-CTA slot stride of yll (>= 16 words)
+  int pstride;           // hidden l>=1: per-CTA row stride of pll (multiple of 16 words)
   float* w;              // [fo][pitch] (output layer: [nct][fo][pitch], one copy per CTA)
-  unsigned long long* yll;  // hidden: [2][fo] flag-carrying activations
-  unsigned long long* pll;  // hidden l>=1: [2][nct][pitch] flag-carrying column partials
+  // Exchange buffers: every CTA's slice starts on its own 128-byte line, so a
+  // polled line has exactly one writer.
+  unsigned long long* yll;  // hidden: [2][P][1<<ylog] flag-carrying activations
+  unsigned long long* pll;  // hidden l>=1: [2][P][pstride] flag-carrying column partials
 };
 
 struct NetDev {
   int L;    // weight layers
   int nct;  // CTAs (row owners)
-  int resident;  // 1: owned rows live in shared memory (DMLP_RES_SMEM)
   int in0_off[2];
   int delta_off[2];
   int dsc_off[2];
-  int red_off;
-  int out_off;
-  int wsm_off;  // smem-resident weights region (floats)
+  int red_off;   // [kWarps] per-warp partial row sums
+  int pbuf_off;  // [4*kThreads] per-row-group column partials
+  int xbuf_off;  // [max_l P_l * R_{l-1}] partials received from every producer
+  int out_off;   // output layer scratch: a | y | delta | eta*delta (kMaxOut each)
   int* err;
-  unsigned long long* prof;  // optional [nct][2] {loop cycles, exchange-wait cycles}
+  unsigned long long* prof;  // optional [nct][kProfWords] phase cycles (0 loop, 1 exchange)
+  unsigned long long* trace;  // optional [nct][64] %globaltimer marks of one sample
+  long long trace_sample;     // which sample of the launch is traced
   LayerDev ly[kMaxLayers];
 };
 
@@ -60,8 +71,10 @@ struct dmlp_net {
   size_t ll_words = 0;
   int* d_err = nullptr;
   int smem_bytes = 0;
+  unsigned resident_mask = 0;
   uint32_t seq = 1;  // next sample sequence number (flag value)
   cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;  // recorded after every operation on the net, whatever the stream
   float* d_stage = nullptr;  // train_step staging: x, y
   uint8_t* d_stage_lab = nullptr;
   long long* d_stage_wrong = nullptr;
@@ -74,6 +87,8 @@ struct dmlp_net {
 namespace dmlp {
 int set_error(int code, const char* fmt, ...);
 int cuda_check(cudaError_t e, const char* what);
+int net_begin(dmlp_net* net, cudaStream_t st);
+int net_end(dmlp_net* net, cudaStream_t st);
 cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
                          const uint8_t* labels, const int32_t* order, long long n, float eta,
                          uint32_t seq0, long long* wrong, float* y_last, cudaStream_t st);

@@ -193,6 +193,7 @@ static int run_eval(dmlp_net* net, const float* x, long long n, float* out, cons
     return rc;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, net->device);
+  if (int rc = net_begin(net, st)) return rc;
   for (long long m0 = 0; m0 < n; m0 += chunk) {
     const int M = (int)((n - m0) < chunk ? (n - m0) : chunk);
     const float* in = x + m0 * net->sizes[0];
@@ -219,7 +220,7 @@ static int run_eval(dmlp_net* net, const float* x, long long n, float* out, cons
                                           guess ? guess + 2 * m0 : nullptr);
     if (int rc = cuda_check(cudaGetLastError(), "eval kernels")) return rc;
   }
-  return DMLP_OK;
+  return net_end(net, st);
 }
 
 }  // namespace dmlp

@@ -42,9 +42,12 @@ class DeviceNet:
         self.device = int(device)
         sizes = (ctypes.c_int32 * len(self.layer_sizes))(*self.layer_sizes)
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().dmlp_net_create(self.device, sizes, len(self.layer_sizes),
-                                              _lib.RESIDENCY[residency], int(n_ctas),
-                                              ctypes.byref(h)), "dmlp_net_create")
+        if isinstance(residency, int):  # explicit resident-layer bitmask
+            code = 0x10000 | residency
+        else:
+            code = _lib.RESIDENCY[residency]
+        _lib.check(_lib.lib().dmlp_net_create(self.device, sizes, len(self.layer_sizes), code,
+                                              int(n_ctas), ctypes.byref(h)), "dmlp_net_create")
         self._h = h
         r, c, t, s = (ctypes.c_int32() for _ in range(4))
         _lib.check(_lib.lib().dmlp_net_info(self._h, ctypes.byref(r), ctypes.byref(c),
@@ -98,14 +101,27 @@ class DeviceNet:
     def profile(self, enable: bool = True) -> None:
         _lib.check(_lib.lib().dmlp_net_profile(self._h, int(bool(enable))), "dmlp_net_profile")
 
+    PROFILE_SLOTS = ("loop", "exchange", "head", "fwd_dot", "fwd_act", "fwd_xchg", "out_dot",
+                     "out_delta", "delta_last", "out_update", "bwd_update", "bwd_xchg",
+                     "upd0", "s13", "s14", "s15")
+
     def read_profile(self) -> dict:
-        """Sums over CTAs since the last read: sample-loop cycles and cycles
-        spent waiting in inter-CTA exchanges ("grid-sync stall")."""
-        a, b = ctypes.c_int64(), ctypes.c_int64()
-        _lib.check(_lib.lib().dmlp_net_read_profile(self._h, ctypes.byref(a), ctypes.byref(b)),
-                   "dmlp_net_read_profile")
-        return {"loop_cycles": a.value, "exchange_cycles": b.value,
-                "exchange_fraction": (b.value / a.value) if a.value else 0.0}
+        """Per-phase cycles summed over CTAs since the last read (thread 0's
+        view), plus the exchange ("grid-sync stall") fraction."""
+        buf = (ctypes.c_int64 * 16)()
+        _lib.check(_lib.lib().dmlp_net_read_profile(self._h, buf), "dmlp_net_read_profile")
+        d = {k: buf[i] for i, k in enumerate(self.PROFILE_SLOTS)}
+        d["exchange_fraction"] = (d["exchange"] / d["loop"]) if d["loop"] else 0.0
+        return d
+
+    def trace(self, sample: int = -1):
+        """Arm a one-sample %globaltimer trace for the next launches (sample
+        >= 0) and return the previous recording as (n_ctas, 64) uint64."""
+        marks = np.zeros((self.n_ctas, 64), dtype=np.uint64)
+        _lib.check(_lib.lib().dmlp_net_trace(self._h, int(sample),
+                                             marks.ctypes.data_as(ctypes.c_void_p)),
+                   "dmlp_net_trace")
+        return marks
 
     # -- training -----------------------------------------------------------------
     def train_step(self, x: np.ndarray, digit: int, eta: float) -> np.ndarray:

@@ -23,10 +23,10 @@ for name in names:
         print(name, "create failed", e); continue
     dn.set_layers(layers)
     prof = len(sys.argv) > 4
-    if prof: dn.profile(True)
     wrong = torch.zeros((), dtype=torch.int64, device="cuda")
     dn.train_epoch(x[:2000], lab[:2000], None, 1e-3, wrong)
     torch.cuda.synchronize()
+    if prof: dn.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); dn.train_epoch(x, lab, None, 1e-3, wrong); e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -35,5 +35,5 @@ for name in names:
     sps = n / (ms / 1e3)
     print(json.dumps({"cfg": name, "res": dn.residency, "nct": dn.n_ctas, "smem": dn.smem_bytes,
                       "us_per_sample": round(ms * 1e3 / n, 3), "samples_s": round(sps),
-                      "GBs_12B": round(12 * W * sps / 1e9, 1), **({"xchg_frac": round(pr["exchange_fraction"], 3), "cyc_per_sample": pr["loop_cycles"] // dn.n_ctas // (n + 2000)} if prof else {})}))
+                      "GBs_12B": round(12 * W * sps / 1e9, 1), **({"xchg_frac": round(pr["exchange_fraction"], 3), "phases_per_sample": {k: v // dn.n_ctas // n for k, v in pr.items() if k not in ("exchange_fraction",) and v}} if prof else {})}))
     dn.close()

@@ -43,7 +43,7 @@ def test_pack_unpack_roundtrip():
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("residency", ["l2", "smem"])
+@pytest.mark.parametrize("residency", ["l2", "smem", 0b101, 0b010])
 def test_train_step_small_vs_golden(golden, residency):
     g = golden("train")
     x, lab = _inputs(golden)
