@@ -1,0 +1,429 @@
+"""Benchmark of the on-line BP hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+A step = one persistent-kernel launch training `--samples` on-line samples
+(batch size 1, sequential) of the C4 net 841-2500-2000-1500-1000-500-10
+(12,115,010 weights) on deformed synthetic digits already resident in HBM.
+`value` = samples/s over the K timed steps (CUDA events on the launching
+stream, barrier + synchronize on both sides, max over ranks).  `e2e` = the
+same metric through the public API (trainer.train_epoch) from pinned host
+buffers: the H2D copy of the step's images/labels/order and the D2H read of
+the error count are inside the timed region.  Extra keys report the
+deformation and evaluation kernels (imgs/s) and the in-kernel profile.
+
+Multi-GPU (torchrun, one rank per GPU): on-line training does not shard
+(SPEC: sample s+1 needs the weights after sample s), so every rank trains an
+independent replica (seed = rank); value = total samples/s of all replicas
+("replicas only", scaling "weak").  Deformation and evaluation shard the
+images; the eval counts are all-reduced with NCCL.
+
+`--impl reference` times the reference algorithm on the host CPU through
+the oracle port (oracle/, bit-exact with the reference package) on a
+bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "C1": (841, 1000, 500, 10),
+    "C2": (841, 1500, 1000, 500, 10),
+    "C3": (841, 2000, 1500, 1000, 500, 10),
+    "C4": (841, 2500, 2000, 1500, 1000, 500, 10),
+    "C5": (841,) + (1000,) * 9 + (10,),
+}
+METRIC = "on-line BP train samples/s (bs=1, 12.11M MLP)"
+
+
+def count_weights(sizes) -> int:
+    return sum((i + 1) * o for i, o in zip(sizes[:-1], sizes[1:]))
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._thr = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._thr.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------- data
+
+
+def make_inputs(n_raw: int, seed: int, device: str):
+    """Synthetic digits -> device, deformed once (epoch 0) by the CUDA kernel."""
+    import numpy as np
+    import torch
+
+    from paper_1003_0358_b200.deform import DeformParams, deform_device
+    from paper_1003_0358_b200.synthetic import make_digits
+
+    images, labels = make_digits(n_raw, seed=12345 + seed)
+    raw = torch.from_numpy(images).to(device)
+    lab = torch.from_numpy(labels).to(device)
+    x = deform_device(raw, lab, DeformParams(), seed, 0)
+    torch.cuda.synchronize()
+    return images, labels, raw, lab, x, np
+
+
+# ----------------------------------------------------------------------------- CPU legs
+
+
+def cpu_train_rate(sizes, seconds: float = 12.0, threads: int | None = None) -> dict:
+    """The reference algorithm (oracle port, bit-exact with kernels.train_step
+    tiled) on the host cores: on-line samples/s over a bounded sample."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_1003_0358_b200.synthetic import make_digits
+
+    threads = threads or os.cpu_count() or 1
+    O.set_threads(threads)
+    imgs, labs = make_digits(64, seed=7)
+    x = O.deform_epoch(imgs, labs, O.DeformParams(), seed=0, epoch=0).reshape(64, -1)
+    layers = O.init_layers(0, sizes)
+    for i in range(3):  # warm-up
+        O.train_step(layers, x[i], int(labs[i]), 1e-3)
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds or n < 5:
+        O.train_step(layers, x[n % 64], int(labs[n % 64]), 1e-3)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"{n} on-line train_step calls of {sizes} in {dt:.1f}s "
+                      f"(oracle/dmlp_oracle.c, tiled arithmetic, {threads} threads)"}
+
+
+def cpu_deform_rate(seconds: float = 4.0, threads: int | None = None) -> dict:
+    from oracle import oracle as O
+    from paper_1003_0358_b200.synthetic import make_digits
+
+    threads = threads or os.cpu_count() or 1
+    imgs, labs = make_digits(2048, seed=3)
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds or n == 0:
+        O.deform_epoch(imgs, labs, O.DeformParams(), seed=0, epoch=n, threads=threads)
+        n += len(imgs)
+    return {"value": n / (time.perf_counter() - t0), "unit": "imgs/s", "cores": threads}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def run_gpu(args) -> dict | None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    device = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(device))
+
+    from paper_1003_0358_b200 import trainer
+    from paper_1003_0358_b200.deform import DeformParams, deform_device, upscale_device
+    from paper_1003_0358_b200.device import DeviceNet
+    from paper_1003_0358_b200.network import Architecture, init_mlp
+    from paper_1003_0358_b200.rng import substream
+
+    sizes = CONFIGS[args.config]
+    W = count_weights(sizes)
+    n = args.samples
+    images, labels, raw, lab, x, _ = make_inputs(n, rank, device)
+    order = torch.from_numpy(substream(rank, 3, 0).permutation(n).astype(np.int32)).to(device)
+
+    mlp = init_mlp(substream(rank, 1), Architecture(sizes))
+    dn = mlp.device_net(local, args.residency)
+    wrong = torch.zeros((), dtype=torch.int64, device=device)
+    stream = torch.cuda.current_stream(device)
+
+    def step():
+        dn.train_epoch(x, lab, order, 1e-3, wrong)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    per_launch_s = ms / 1e3 / args.steps
+    sps_rank = n / per_launch_s
+    value = world * n * args.steps / (ms_max / 1e3)
+
+    # ---- in-kernel phase profile on one extra (untimed) launch
+    dn.profile(True)
+    step()
+    torch.cuda.synchronize(device)
+    prof = dn.read_profile()
+    dn.profile(False)
+
+    # ---- end to end through the public API, host (pinned) buffers
+    x_host = torch.empty((n, 841), dtype=torch.float32).pin_memory()
+    x_host.copy_(x.cpu())
+    lab_host = torch.from_numpy(labels).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        trainer.train_epoch(mlp, x_host, lab_host, 1e-3, rng=substream(rank, 3, s))
+    barrier()
+    e2e_dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_dt], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_dt = float(t.item())
+    e2e = {"value": world * n * e2e_steps / e2e_dt, "unit": "samples/s",
+           "h2d_bytes_per_step": n * 841 * 4 + n + n * 4, "d2h_bytes_per_step": 8,
+           "api": "paper_1003_0358_b200.trainer.train_epoch(mlp, pinned host images, "
+                  "labels, eta, rng)"}
+
+    # ---- deformation kernel: the whole epoch's images, sharded by rank
+    nd = args.deform_images
+    d_imgs = torch.from_numpy(np.resize(images, (nd, 28, 28))).to(device)
+    d_lab = torch.from_numpy(np.resize(labels, nd)).to(device)
+    lo, hi = rank * nd // world, (rank + 1) * nd // world
+    d_out = torch.empty((hi - lo, 841), dtype=torch.float32, device=device)
+    for _ in range(2):
+        deform_device(d_imgs[lo:hi], d_lab[lo:hi], DeformParams(), 0, 1, first=lo, out=d_out)
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for e in range(3):
+        deform_device(d_imgs[lo:hi], d_lab[lo:hi], DeformParams(), 0, 2 + e, first=lo, out=d_out)
+    b.record(stream)
+    barrier()
+    dms = a.elapsed_time(b) / 3
+    if world > 1:
+        t = torch.tensor([dms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dms = float(t.item())
+    deform = {"imgs_per_s": nd / (dms / 1e3), "images": nd, "ms_per_epoch": round(dms, 3),
+              "bytes_per_img": 4149, "GBs": round(4149 * nd / (dms / 1e3) / 1e9, 1)}
+
+    # ---- evaluation: validation pass over the un-deformed training images
+    ev = DeviceNet(sizes, device=local)
+    ev.set_layers(mlp.layers)
+    xv = upscale_device(d_imgs[lo:hi])
+    counts = torch.zeros(102, dtype=torch.int64, device=device)
+    ev.eval_counts(xv, d_lab[lo:hi], counts)
+    barrier()
+    a.record(stream)
+    ev.eval_counts(xv, d_lab[lo:hi], counts)
+    b.record(stream)
+    if world > 1:
+        dist.all_reduce(counts)  # the single NCCL all-reduce of the count vector
+    barrier()
+    ems = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ems], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    flops = 2 * sum(i * o for i, o in zip(sizes[:-1], sizes[1:]))
+    evaluation = {"imgs_per_s": nd / (ems / 1e3), "images": nd,
+                  "TFLOPs": round(flops * nd / (ems / 1e3) / 1e12, 2)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    peaks = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = 12.0 * W * sps_rank / 1e9
+    l2 = l2_peak()
+    traffic = profiled_traffic(args.config)
+    roofline = {
+        "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+        "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+        "algorithmic_bytes_per_sample": 12 * W,
+        "residency": dn.residency,
+        "l2_peak_rw_GBs": l2, "frac_of_l2_rw": round(achieved / l2, 4) if l2 else None,
+        "exchange_fraction": round(prof["exchange_fraction"], 3),
+    }
+    cpu = cpu_train_rate(sizes, seconds=args.cpu_seconds) if args.cpu_seconds > 0 else None
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} {'-'.join(map(str, sizes))} on-line BP "
+                               f"(bs=1), {n} deformed synthetic digits per step",
+                   "weights": W, "samples_per_step": n,
+                   "parallelism": "replicas only" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (n*841*4 B per step); weights are "
+                         "deliberately kept in smem/L2"},
+        "e2e": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in e2e.items()},
+        "gpu_launches": args.steps,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "deform": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in deform.items()},
+        "eval": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in evaluation.items()},
+        "profile_cycles_per_sample": {k: v // max(1, dn.n_ctas) // n for k, v in prof.items()
+                                      if k != "exchange_fraction" and v},
+    }
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def l2_peak() -> float | None:
+    """K6: L2-resident read+write bandwidth (48 MB, one CTA per SM)."""
+    try:
+        from paper_1003_0358_b200 import microbench
+
+        s, _ = microbench.run(1, 48 << 20, 10)
+        return round(2 * (48 << 20) * 10 / s / 1e9, 1)
+    except Exception:
+        return None
+
+
+def profiled_traffic(cfg: str):
+    """dram bytes per launch from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", f"ncu_train_{cfg.lower()}.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+
+def run_reference(args) -> dict | None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    sizes = CONFIGS[args.config]
+    W = count_weights(sizes)
+    per = max(2.0, args.cpu_seconds)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_train_rate(sizes, seconds=per / 4)
+    for _ in range(args.steps):
+        vals.append(cpu_train_rate(sizes, seconds=per)["value"])
+    v = statistics.median(vals)
+    cpu = cpu_train_rate(sizes, seconds=1.0)
+    cpu["value"] = v
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * per, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} {'-'.join(map(str, sizes))} on-line BP (bs=1)",
+                   "weights": W},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(v, 3), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "reference algorithm = oracle/dmlp_oracle.c (bit-exact with the reference "
+                "kernels.train_step tiled variant, pinned by tests/test_oracle_golden.py); the "
+                "Python/numba reference itself cannot travel to the GPU host",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--samples", type=int, default=20000, help="on-line samples per step")
+    ap.add_argument("--deform-images", type=int, default=60000)
+    ap.add_argument("--residency", default="auto")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    line = run_reference(args) if args.impl == "reference" else run_gpu(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -23,30 +23,62 @@
 
 #include <pthread.h>
 
-/* Minimal fork/join parallel-for over [0, n) with static chunks (replaces
- * numba's prange; every index's arithmetic is independent of the split). */
+/* Persistent fork/join pool: parallel-for over [0, n) in static chunks
+ * (replaces numba's prange; every index's arithmetic is independent of the
+ * split, so results do not depend on the thread count). */
 static int g_threads = 1;
 typedef void (*or_body_fn)(void *ctx, int64_t lo, int64_t hi);
-typedef struct { or_body_fn fn; void *ctx; int64_t lo, hi; } or_task;
-static void *or_task_run(void *p) {
-  or_task *t = (or_task *)p;
-  t->fn(t->ctx, t->lo, t->hi);
+#define OR_MAX_THREADS 256
+static pthread_mutex_t g_mu = PTHREAD_MUTEX_INITIALIZER;
+static pthread_cond_t g_cv_go = PTHREAD_COND_INITIALIZER, g_cv_done = PTHREAD_COND_INITIALIZER;
+static int g_pool_size = 0;          /* worker threads started (excl. caller) */
+static unsigned long g_gen = 0;      /* task generation */
+static int g_pending = 0;            /* workers still running the task */
+static or_body_fn g_fn;
+static void *g_ctx;
+static int64_t g_n;
+static int g_T;                      /* participants of the current task */
+
+static void *or_worker(void *arg) {
+  const int id = (int)(intptr_t)arg; /* 1..pool */
+  unsigned long seen = 0;
+  for (;;) {
+    pthread_mutex_lock(&g_mu);
+    while (g_gen == seen) pthread_cond_wait(&g_cv_go, &g_mu);
+    seen = g_gen;
+    const int T = g_T;
+    or_body_fn fn = g_fn;
+    void *ctx = g_ctx;
+    const int64_t n = g_n;
+    pthread_mutex_unlock(&g_mu);
+    if (id < T) fn(ctx, n * id / T, n * (id + 1) / T);
+    pthread_mutex_lock(&g_mu);
+    if (--g_pending == 0) pthread_cond_signal(&g_cv_done);
+    pthread_mutex_unlock(&g_mu);
+  }
   return NULL;
 }
+
 static void or_parallel_for(int64_t n, or_body_fn fn, void *ctx) {
   int T = g_threads;
-  if (T <= 1 || n < 2) { fn(ctx, 0, n); return; }
   if (T > n) T = (int)n;
-  pthread_t th[256];
-  or_task tk[256];
-  if (T > 256) T = 256;
-  for (int k = 0; k < T; k++) {
-    tk[k].fn = fn; tk[k].ctx = ctx;
-    tk[k].lo = n * k / T; tk[k].hi = n * (k + 1) / T;
+  if (T <= 1) { fn(ctx, 0, n); return; }
+  pthread_mutex_lock(&g_mu);
+  while (g_pool_size < T - 1 && g_pool_size < OR_MAX_THREADS - 1) {
+    pthread_t th;
+    g_pool_size++;
+    pthread_create(&th, NULL, or_worker, (void *)(intptr_t)g_pool_size);
+    pthread_detach(th);
   }
-  for (int k = 1; k < T; k++) pthread_create(&th[k], NULL, or_task_run, &tk[k]);
-  or_task_run(&tk[0]);
-  for (int k = 1; k < T; k++) pthread_join(th[k], NULL);
+  g_fn = fn; g_ctx = ctx; g_n = n; g_T = T;
+  g_pending = g_pool_size;
+  g_gen++;
+  pthread_cond_broadcast(&g_cv_go);
+  pthread_mutex_unlock(&g_mu);
+  fn(ctx, 0, n / T);
+  pthread_mutex_lock(&g_mu);
+  while (g_pending > 0) pthread_cond_wait(&g_cv_done, &g_mu);
+  pthread_mutex_unlock(&g_mu);
 }
 
 #define OR_A 1.7159f   /* network.py:13 */
@@ -409,6 +441,6 @@ void or_fp_naive(const float *w, int fo, int fi, const float *x, float *a, float
 float or_tanhf(float x) { return tanhf(x); }
 
 int or_set_threads(int n) {
-  if (n > 0) g_threads = n > 256 ? 256 : n;
+  if (n > 0) g_threads = n > OR_MAX_THREADS ? OR_MAX_THREADS : n;
   return g_threads;
 }
