@@ -314,12 +314,13 @@ def run_gpu(args) -> dict | None:
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = 12.0 * W * sps_rank / 1e9
     l2 = l2_peak()
-    traffic = profiled_traffic(args.config)
+    traffic = profiled_traffic(args.config, n)
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
         "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
         "algorithmic_bytes_per_sample": 12 * W,
+        "algorithmic_bytes_per_launch": 12 * W * n,
         "residency": dn.residency,
         "l2_peak_rw_GBs": l2, "frac_of_l2_rw": round(achieved / l2, 4) if l2 else None,
         "exchange_fraction": round(prof["exchange_fraction"], 3),
@@ -362,12 +363,13 @@ def l2_peak() -> float | None:
         return None
 
 
-def profiled_traffic(cfg: str):
-    """dram bytes per launch from the committed ncu capture, if any."""
+def profiled_traffic(cfg: str, samples: int):
+    """DRAM bytes (read + write) per launch of `samples` samples, scaled from
+    the committed `ncu --set full` capture of the same kernel and config."""
     p = os.path.join(ROOT, "profiles", f"ncu_train_{cfg.lower()}.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return round(json.load(f)["dram_bytes_per_unit"] * samples)
     except Exception:
         return None
 
