@@ -50,16 +50,13 @@ int net_end(dmlp_net* net, cudaStream_t st) {
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-// Reference layout (fo, fi+1) row-major -> device rows of `pitch` floats,
-// replicated `copies` times (the output layer keeps one copy per CTA).
+// Reference layout (fo, fi+1) row-major -> device rows of `pitch` floats.
 __global__ void k_pack(const float* __restrict__ src, float* __restrict__ dst, int fo, int fi,
-                       int pitch, int copies) {
-  const long long per = (long long)fo * pitch;
-  const long long total = per * copies;
+                       int pitch) {
+  const long long total = (long long)fo * pitch;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    const long long r = t % per;
-    const int j = (int)(r / pitch), i = (int)(r % pitch);
+    const int j = (int)(t / pitch), i = (int)(t % pitch);
     dst[t] = (i <= fi) ? src[(long long)j * (fi + 1) + i] : 0.0f;
   }
 }
@@ -82,60 +79,71 @@ static int ceil_log2(int x) {
   return l;
 }
 
-// Lay out dynamic shared memory for a resident-layer mask; returns bytes.
+// Lay out dynamic shared memory for a resident-layer mask (hidden layers);
+// returns bytes.
 static int layout_smem(dmlp_net* net, unsigned mask) {
   NetDev& d = net->dev;
-  const int L = d.L;
+  const int L = d.L, H = L - 1;
   int off = 0;
   auto take = [&](int floats) {
     const int o = off;
-    off += round_up(floats, 4);
+    off += round_up(floats > 0 ? floats : 1, 4);
     return o;
   };
   d.in0_off[0] = take(d.ly[0].pitch);
   d.in0_off[1] = take(d.ly[0].pitch);
-  for (int l = 1; l < L; l++) d.ly[l].in_off = take(d.ly[l].pitch);
   d.ly[0].in_off = d.in0_off[0];
-  int maxr = 1;
-  for (int l = 0; l < L - 1; l++) {
-    const int r = own_max_rows(d.ly[l].fo, d.nct);
-    d.ly[l].t_off = take(r);
-    if (r > maxr) maxr = r;
+  for (int l = 1; l < H; l++) d.ly[l].in_off = take(d.ly[l].pitch);
+  int maxr = 1, pb = 1;
+  for (int l = 0; l < H; l++) {
+    d.ly[l].t_off = take(d.ly[l].R);
+    if (d.ly[l].R > maxr) maxr = d.ly[l].R;
+    const int G = 1 << d.ly[l].gs;
+    if (G > 1 && G * d.ly[l].pitch > pb) pb = G * d.ly[l].pitch;
   }
-  d.ly[L - 1].t_off = 0;
+  d.yown_off = take(H > 0 ? d.ly[H - 1].R : 1);
   for (int b = 0; b < 2; b++) {
     d.delta_off[b] = take(maxr);
     d.dsc_off[b] = take(maxr);
   }
   d.red_off = take(kWarps * 32);
-  d.pbuf_off = take(4 * kThreads);
-  int xb = 1;
-  for (int l = 1; l < L - 1; l++) {
-    const int need = d.ly[l].P * d.ly[l - 1].R;
-    if (need > xb) xb = need;
-  }
-  d.xbuf_off = take(xb);
+  d.pbuf_off = take(pb);
   d.out_off = take(4 * kMaxOut);
-  for (int l = 0; l < L; l++) {
+  LayerDev& lo = d.ly[L - 1];
+  lo.res = 1;
+  lo.wsm_off = take(lo.fo * (lo.R + 1));
+  for (int l = 0; l < H; l++) {
     d.ly[l].res = (mask >> l) & 1u;
-    d.ly[l].wsm_off = 0;
-    if (d.ly[l].res) {
-      const int r = (l < L - 1) ? own_max_rows(d.ly[l].fo, d.nct) : d.ly[l].fo;
-      d.ly[l].wsm_off = take(r * d.ly[l].pitch);
-    }
+    d.ly[l].wsm_off = d.ly[l].res ? take(d.ly[l].R * d.ly[l].pitch) : 0;
   }
   return off * (int)sizeof(float);
 }
 
-// Resident-layer mask for a residency policy: all, none, or (AUTO) the subset
-// that keeps the most weight bytes on chip within the smem budget.
 static long long resident_floats(const NetDev& d, unsigned mask) {
   long long f = 0;
-  for (int l = 0; l < d.L; l++)
-    if ((mask >> l) & 1u)
-      f += (long long)((l < d.L - 1) ? own_max_rows(d.ly[l].fo, d.nct) : d.ly[l].fo) *
-           d.ly[l].pitch;
+  for (int l = 0; l < d.L - 1; l++)
+    if ((mask >> l) & 1u) f += (long long)d.ly[l].R * d.ly[l].pitch;
   return f;
+}
+
+// Thread mapping of a hidden layer's row block (LayerDev): the row-group
+// count G = 2^gs minimising the serial steps ceil(R/G) * ceil(quads/(512/G))
+// (plus reduction chunks), and the reduction chunk CH >= rows per group
+// (capped at 16: chunks beyond).
+static void choose_mapping(LayerDev& ly) {
+  const int nq = ly.pitch / 4;
+  int best = 1 << 30;
+  for (int gs = 0; (1 << gs) <= kWarps; gs++) {
+    const int G = 1 << gs, TG = kThreads / G;
+    const int C = (nq + TG - 1) / TG, nj = (ly.R + G - 1) / G;
+    const int cost = C * nj + (G > 1 ? 2 : 0) + 8 * ((nj + 15) / 16 - 1);
+    if (cost < best) {
+      best = cost;
+      ly.gs = gs;
+    }
+  }
+  const int nj = (ly.R + (1 << ly.gs) - 1) >> ly.gs;
+  ly.CH = nj <= 4 ? 4 : nj <= 8 ? 8 : 16;
 }
 
 }  // namespace dmlp
@@ -186,7 +194,9 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
   d.L = n_sizes - 1;
   int nct = n_ctas > 0 ? n_ctas : prop.multiProcessorCount;
   if (nct > prop.multiProcessorCount) nct = prop.multiProcessorCount;
+  if (d.L == 1) nct = 1;  // no hidden layer: nothing to distribute
   d.nct = nct;
+  const int H = d.L - 1;
 
   size_t woff = 0;
   for (int l = 0; l < d.L; l++) {
@@ -194,9 +204,8 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     h.fi = sizes[l];
     h.fo = sizes[l + 1];
     h.pitch = round_up(h.fi + 1, 4);
-    h.copies = (l == d.L - 1) ? (size_t)nct : 1;
     h.w_off = woff;
-    woff += (size_t)h.fo * h.pitch * h.copies;
+    woff += (size_t)h.fo * h.pitch;
     d.ly[l].fi = h.fi;
     d.ly[l].fo = h.fo;
     d.ly[l].pitch = h.pitch;
@@ -204,32 +213,40 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
   net->w_floats = woff;
 
   // exchange buffers (line-aligned per producer): y words [2][P][1<<ylog] for
-  // hidden layers, partial words [2][P][pstride] for hidden layers l >= 1
+  // hidden layers but the last, output partials [2][P][1<<ylog], column
+  // partial words [2][P][pstride] for hidden layers l >= 1
   size_t ll = 0;
   size_t yoff[kMaxLayers], poff[kMaxLayers];
-  for (int l = 0; l < d.L - 1; l++) {
+  for (int l = 0; l < H; l++) {
     LayerDev& ly = d.ly[l];
     ly.R = own_max_rows(ly.fo, nct);
-    if (ly.R > 4 * kThreads) {
-      delete net;
-      return set_error(DMLP_EINVAL, "layer %d: %d rows per CTA exceed the staging buffer", l,
-                       ly.R);
-    }
     ly.P = (ly.fo + ly.R - 1) / ly.R;
     ly.ylog = ceil_log2(ly.R < 16 ? 16 : ly.R);
     ly.pstride = round_up(ly.fi, 16);
+    choose_mapping(ly);
     yoff[l] = ll;
-    ll += 2 * (size_t)ly.P << ly.ylog;
+    if (l < H - 1) ll += 2 * (size_t)ly.P << ly.ylog;
     if (l >= 1) {
       poff[l] = ll;
       ll += 2 * (size_t)ly.P * ly.pstride;
     }
   }
+  {
+    LayerDev& lo = d.ly[d.L - 1];
+    lo.R = H > 0 ? d.ly[H - 1].R : lo.fi;  // owned input columns per CTA
+    lo.P = H > 0 ? d.ly[H - 1].P : 1;
+    lo.ylog = ceil_log2(lo.fo < 16 ? 16 : lo.fo);
+    lo.gs = 0;
+    lo.CH = 1;
+    lo.pstride = 0;
+    yoff[d.L - 1] = ll;
+    ll += 2 * (size_t)lo.P << lo.ylog;
+  }
   net->ll_words = ll;
 
   // residency: choose which layers keep their rows in shared memory
   const int smem_cap = (int)prop.sharedMemPerBlockOptin - 1024;  // keep room for static smem
-  const unsigned all = (d.L >= 32) ? 0xFFFFFFFFu : ((1u << d.L) - 1u);
+  const unsigned all = (1u << H) - 1u;  // hidden layers (the output tile is always resident)
   unsigned mask = 0;
   if (residency & DMLP_RES_MASK) {
     mask = (unsigned)residency & all;
@@ -302,8 +319,8 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     return fail(rc);
   for (int l = 0; l < d.L; l++) {
     d.ly[l].w = net->d_w + net->hl[l].w_off;
-    d.ly[l].yll = (l < d.L - 1) ? net->d_ll + yoff[l] : nullptr;
-    d.ly[l].pll = (l >= 1 && l < d.L - 1) ? net->d_ll + poff[l] : nullptr;
+    d.ly[l].yll = (l < H - 1 || l == d.L - 1) ? net->d_ll + yoff[l] : nullptr;
+    d.ly[l].pll = (l >= 1 && l < H) ? net->d_ll + poff[l] : nullptr;
   }
   d.err = net->d_err;
   d.prof = nullptr;
@@ -415,8 +432,7 @@ int dmlp_net_set_layer(dmlp_net* net, int32_t layer, const float* w, int64_t n) 
   DMLP_CUDA(cudaStreamWaitEvent(net->stream, net->done, 0));
   DMLP_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), net->stream));
   DMLP_CUDA(cudaMemcpyAsync(tmp, w, n * sizeof(float), cudaMemcpyDefault, net->stream));
-  k_pack<<<296, 256, 0, net->stream>>>(tmp, net->d_w + h.w_off, h.fo, h.fi, h.pitch,
-                                       (int)h.copies);
+  k_pack<<<296, 256, 0, net->stream>>>(tmp, net->d_w + h.w_off, h.fo, h.fi, h.pitch);
   DMLP_CUDA(cudaGetLastError());
   DMLP_CUDA(cudaFreeAsync(tmp, net->stream));
   DMLP_CUDA(cudaEventRecord(net->done, net->stream));

@@ -12,25 +12,36 @@ namespace dmlp {
 constexpr int kThreads = 512;  // threads per CTA of the persistent kernel
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLayers = 16;
-constexpr int kMaxOut = 32;  // replicated output layer: at most 32 classes
+constexpr int kMaxOut = 32;  // output layer: at most 32 classes
 constexpr int kProfWords = 16;  // profile slots per CTA
 
-// One weight layer as the persistent kernel sees it.
+// One weight layer as the persistent kernel sees it (DESIGN.md §3.1).
+//
+// Hidden layer l: CTA c owns the row block [c*R, min(c*R+R, fo)).  Inside a
+// CTA the 512 threads form G = 2^gs row groups of TG = 512/G threads; thread
+// (g, u) handles rows g, g+G, ... and the float4 column quads u, u+TG, ...,
+// so every phase (forward dot, column partials, update) keeps all threads
+// busy and walks a row with consecutive lanes on consecutive quads.
+// Output layer: CTA c owns the COLUMNS of W_out that match its rows of the
+// last hidden layer (CTA 0 also the bias column); its [fo][R+1] tile lives
+// in shared memory for the whole launch.
 struct LayerDev {
   int fi, fo, pitch;     // fan-in, fan-out, floats per device row (>= fi+1, %4 == 0)
-  int in_off;            // smem offset (floats) of this layer's input vector (pitch long)
-  int t_off;             // smem offset of the owned rows' tanh(B*a) cache
-  int res;               // 1: the CTA's rows of this layer live in shared memory
-  int wsm_off;           // resident: smem offset of the owned rows (or the output copy)
-  int R;                 // hidden: rows per CTA block; CTA c owns [c*R, min(c*R+R, fo))
-  int P;                 // hidden: CTAs owning at least one row = ceil(fo / R)
-  int ylog;              // hidden: log2 of the per-CTA slot stride of yll (>= 16 words)
+  int in_off;            // hidden l >= 1: smem offset of the gathered input vector (pitch long)
+  int t_off;             // hidden: smem offset of the owned rows' tanh(B*a) cache
+  int res;               // hidden: 1 = the CTA's rows live in shared memory, 0 = streamed (L2)
+  int wsm_off;           // resident hidden rows / output tile: smem offset
+  int R;                 // hidden: rows per CTA block; output: owned input columns per CTA
+  int P;                 // CTAs owning at least one row (output: producing a partial)
+  int gs, CH;            // hidden: log2 of the row groups G, rows per reduction chunk
+  int ylog;              // log2 words per producer slot of yll (>= 16 words, line aligned)
   int pstride;           // hidden l>=1: per-CTA row stride of pll (multiple of 16 words)
-  float* w;              // [fo][pitch] (output layer: [nct][fo][pitch], one copy per CTA)
+  float* w;              // [fo][pitch], reference order, bias in column fi
   // Exchange buffers: every CTA's slice starts on its own 128-byte line, so a
-  // polled line has exactly one writer (DESIGN.md §3.3).
-  unsigned long long* yll;  // hidden: [2][P][1<<ylog] flag-carrying activations
-  unsigned long long* pll;  // hidden l>=1: [2][P][pstride] flag-carrying column partials
+  // polled line has exactly one writer (DESIGN.md §3.1).
+  unsigned long long* yll;  // hidden l < L-2: [2][P][1<<ylog] activations;
+                            // output: [2][P][1<<ylog] partial pre-activations
+  unsigned long long* pll;  // hidden l>=1: [2][P][pstride] column partials
 };
 
 struct NetDev {
@@ -39,9 +50,9 @@ struct NetDev {
   int in0_off[2];
   int delta_off[2];
   int dsc_off[2];
-  int red_off;   // [kWarps] per-warp partial row sums
-  int pbuf_off;  // [4*kThreads] per-row-group column partials
-  int xbuf_off;  // [max_l P_l * R_{l-1}] partials received from every producer
+  int yown_off;  // [R] y of the owned rows of the last hidden layer
+  int red_off;   // [kWarps][32] reduction scratch
+  int pbuf_off;  // [Gmax][pitch] per-row-group column partials (G > 1 layers)
   int out_off;   // output layer scratch: a | y | delta | eta*delta (kMaxOut each)
   int* err;
   unsigned long long* prof;  // optional [nct][kProfWords] phase cycles (0 loop, 1 exchange)
@@ -53,7 +64,6 @@ struct NetDev {
 struct HostLayer {
   int fi, fo, pitch;
   size_t w_off;  // float offset into the weights allocation
-  size_t copies; // 1, or nct for the replicated output layer
 };
 
 }  // namespace dmlp

@@ -101,9 +101,9 @@ class DeviceNet:
     def profile(self, enable: bool = True) -> None:
         _lib.check(_lib.lib().dmlp_net_profile(self._h, int(bool(enable))), "dmlp_net_profile")
 
-    PROFILE_SLOTS = ("loop", "exchange", "head", "fwd_dot", "fwd_act", "fwd_xchg", "out_dot",
-                     "out_delta", "delta_last", "out_update", "bwd_update", "bwd_xchg",
-                     "upd0", "s13", "s14", "s15")
+    PROFILE_SLOTS = ("loop", "exchange", "head", "fwd", "fwd_xchg", "out_part", "out_xchg",
+                     "out_stage", "bwd_part", "bwd_upd", "bwd_xchg", "upd0", "s12", "s13", "s14",
+                     "s15")
 
     def read_profile(self) -> dict:
         """Per-phase cycles summed over CTAs since the last read (thread 0's
