@@ -345,7 +345,10 @@ def run_gpu(args) -> dict | None:
         "deform": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in deform.items()},
         "eval": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in evaluation.items()},
         "profile_cycles_per_sample": {k: v // max(1, dn.n_ctas) // n for k, v in prof.items()
-                                      if k != "exchange_fraction" and v},
+                                      if k not in ("exchange_fraction", "layers") and v},
+        "profile_cycles_per_layer": [
+            {k: v // max(1, dn.n_ctas) // n for k, v in lay.items()} for lay in prof["layers"]],
+        "layer_residency": dn.layer_residency,
     }
     if world > 1:
         dist.destroy_process_group()

@@ -35,6 +35,7 @@ extern "C" {
 #define DMLP_RES_SMEM 2   /* every CTA keeps its owned rows in shared memory */
 #define DMLP_RES_HYBRID 3 /* (reported only) some layers resident, the rest streamed */
 #define DMLP_RES_MASK 0x10000 /* DMLP_RES_MASK | m: exactly the layers in bitmask m resident */
+#define DMLP_RES_NOREG 0x20000 /* with AUTO: shared memory / L2 only, no register row blocks */
 
 typedef struct dmlp_net dmlp_net;
 
@@ -65,6 +66,11 @@ int dmlp_net_destroy(dmlp_net *net);
 int dmlp_net_info(dmlp_net *net, int32_t *residency, int32_t *n_ctas, int32_t *threads,
                   int32_t *smem_bytes);
 
+/* Where each weight layer's owned rows live in the training kernel:
+ * where[l] = 0 streamed from L2 every sample, 1 shared memory, 2 registers
+ * (n_layers entries; the output layer's column tile is always in smem). */
+int dmlp_net_layer_residency(dmlp_net *net, int32_t *where);
+
 /* Pack one layer from the reference layout (fo, fi+1) row-major, bias last
  * (network.py:61-64), host or device pointer, n = fo*(fi+1) floats. */
 int dmlp_net_set_layer(dmlp_net *net, int32_t layer, const float *w, int64_t n);
@@ -77,6 +83,10 @@ int dmlp_net_get_layer(dmlp_net *net, int32_t layer, float *w, int64_t n);
  * 1 = cycles waiting in inter-CTA exchanges, 2.. = phases. */
 int dmlp_net_profile(dmlp_net *net, int32_t enable);
 int dmlp_net_read_profile(dmlp_net *net, int64_t *slots);
+/* The same plus the per-layer split: slots[16 + 5*l + k] for weight layer l,
+ * k = 0 forward, 1 gather of its input, 2 column partials, 3 update,
+ * 4 gather of the partials by the layer below.  Fills n_slots (<= 96). */
+int dmlp_net_read_profile_all(dmlp_net *net, int64_t *slots, int32_t n_slots);
 /* One-sample timeline of the next launches: every CTA records %globaltimer
  * at 64 marks of sample `sample` (mark 0 start; for exchange e, 1+2e = its
  * contribution published, 2+2e = its gather done; 63 end).  marks (optional,
@@ -144,6 +154,12 @@ int dmlp_bench(int32_t kind, int64_t bytes, int32_t iters, int32_t n_ctas, doubl
  * threads), [1] exact scaled tanh, [2] IEEE fp32 divide, [3] warp shuffle
  * reduction, [4] dependent L2 load, [5] dependent ld.relaxed.gpu, [6] smem load. */
 int dmlp_bench_prims(double *out);
+
+/* Device tanhf checks: the select-form kernel tanhf against its branchy
+ * glibc restatement on all 2^32 inputs (NaN payloads aside), and evaluation
+ * on given inputs (device pointers) for comparison with the host libm. */
+int dmlp_tanhf_check(uint64_t *mismatches, uint32_t *first_bad);
+int dmlp_tanhf_eval(const float *x_dev, float *y_dev, int64_t n);
 
 #ifdef __cplusplus
 }

@@ -39,8 +39,10 @@ SIGNATURES = [
     ("dmlp_net_create", ctypes.c_int, [ctypes.c_int, I32P, i32, i32, i32, ctypes.POINTER(P)]),
     ("dmlp_net_destroy", ctypes.c_int, [P]),
     ("dmlp_net_info", ctypes.c_int, [P, I32P, I32P, I32P, I32P]),
+    ("dmlp_net_layer_residency", ctypes.c_int, [P, I32P]),
     ("dmlp_net_profile", ctypes.c_int, [P, i32]),
     ("dmlp_net_read_profile", ctypes.c_int, [P, I64P]),
+    ("dmlp_net_read_profile_all", ctypes.c_int, [P, I64P, i32]),
     ("dmlp_net_trace", ctypes.c_int, [P, i64, P]),
     ("dmlp_net_set_layer", ctypes.c_int, [P, i32, P, i64]),
     ("dmlp_net_get_layer", ctypes.c_int, [P, i32, P, i64]),
@@ -54,6 +56,9 @@ SIGNATURES = [
     ("dmlp_bench", ctypes.c_int, [i32, i64, i32, i32, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double)]),
     ("dmlp_bench_prims", ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
+    ("dmlp_tanhf_check", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64),
+                                        ctypes.POINTER(ctypes.c_uint32)]),
+    ("dmlp_tanhf_eval", ctypes.c_int, [P, P, i64]),
 ]
 
 _lib = None

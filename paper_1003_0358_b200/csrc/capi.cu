@@ -81,7 +81,8 @@ static int ceil_log2(int x) {
 
 // Lay out dynamic shared memory for a resident-layer mask (hidden layers);
 // returns bytes.
-static int layout_smem(dmlp_net* net, unsigned mask) {
+static int layout_smem(dmlp_net* net, unsigned mask, unsigned regmask = 0,
+                       int reg_tail_floats = 0) {
   NetDev& d = net->dev;
   const int L = d.L, H = L - 1;
   int off = 0;
@@ -98,8 +99,9 @@ static int layout_smem(dmlp_net* net, unsigned mask) {
   for (int l = 0; l < H; l++) {
     d.ly[l].t_off = take(d.ly[l].R);
     if (d.ly[l].R > maxr) maxr = d.ly[l].R;
-    const int G = 1 << d.ly[l].gs;
-    if (G > 1 && G * d.ly[l].pitch > pb) pb = G * d.ly[l].pitch;
+    const int G = 1 << d.ly[l].gs;  // column-partial staging: layers with a backward pass
+    if (l >= 1 && !((regmask >> l) & 1u) && G > 1 && G * d.ly[l].pitch > pb)
+      pb = G * d.ly[l].pitch;
   }
   d.yown_off = take(H > 0 ? d.ly[H - 1].R : 1);
   for (int b = 0; b < 2; b++) {
@@ -113,8 +115,9 @@ static int layout_smem(dmlp_net* net, unsigned mask) {
   lo.res = 1;
   lo.wsm_off = take(lo.fo * (lo.R + 1));
   for (int l = 0; l < H; l++) {
-    d.ly[l].res = (mask >> l) & 1u;
-    d.ly[l].wsm_off = d.ly[l].res ? take(d.ly[l].R * d.ly[l].pitch) : 0;
+    d.ly[l].res = ((regmask >> l) & 1u) ? kResReg : ((mask >> l) & 1u) ? kResSmem : kResL2;
+    d.ly[l].wsm_off = d.ly[l].res == kResSmem ? take(d.ly[l].R * d.ly[l].pitch)
+                      : d.ly[l].res == kResReg ? take(reg_tail_floats) : 0;
   }
   return off * (int)sizeof(float);
 }
@@ -136,6 +139,9 @@ static void choose_mapping(LayerDev& ly) {
   for (int gs = 0; (1 << gs) <= kWarps; gs++) {
     const int G = 1 << gs, TG = kThreads / G;
     const int C = (nq + TG - 1) / TG, nj = (ly.R + G - 1) / G;
+    // G > 1 stages G partial vectors in smem for the backward pass: only for
+    // narrow layers, where the staging costs little shared memory
+    if (G > 1 && G * ly.pitch > 2048) break;
     const int cost = C * nj + (G > 1 ? 2 : 0) + 8 * ((nj + 15) / 16 - 1);
     if (cost < best) {
       best = cost;
@@ -177,6 +183,8 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     if (sizes[i] < 1) return set_error(DMLP_EINVAL, "layer sizes must be positive");
   if (sizes[n_sizes - 1] > kMaxOut)
     return set_error(DMLP_EINVAL, "output layer wider than %d is not supported", kMaxOut);
+  const bool noreg = (residency & DMLP_RES_NOREG) != 0;
+  residency &= ~DMLP_RES_NOREG;
   if ((residency < DMLP_RES_AUTO || residency > DMLP_RES_SMEM) && !(residency & DMLP_RES_MASK))
     return set_error(DMLP_EINVAL, "unknown residency %d", residency);
   DMLP_CUDA(cudaSetDevice(device));
@@ -266,12 +274,55 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
                        need, smem_cap);
     }
   } else if (residency == DMLP_RES_AUTO) {
+    // Keep the most weight bytes on chip: for every compiled register plan,
+    // put its row blocks on the largest layers that fit them, then pick the
+    // best shared-memory subset of the rest.  Ties go to the simpler plan.
     long long best = -1;
-    for (unsigned m = 0; m <= all; m++) {
-      if (layout_smem(net, m) > smem_cap) continue;
-      const long long f = resident_floats(d, m);
-      if (f > best) { best = f; mask = m; }
+    const TrainVariant* vars = nullptr;
+    const int nv = train_variants(&vars);
+    for (int vi = 0; vi < nv; vi++) {
+      const TrainVariant& tv = vars[vi];
+      if (noreg && tv.n_reg > 0) continue;
+      unsigned regmask = 0;
+      long long regf = 0;
+      for (int i = 0; i < tv.n_reg; i++) {  // greedy: largest fitting layer not yet taken
+        int pick = -1;
+        long long pf = 0;
+        for (int l = 0; l < H; l++) {
+          const LayerDev& ly = d.ly[l];
+          if (((regmask >> l) & 1u) || ly.R > tv.rr || ly.pitch > kThreads * (tv.rc + tv.rs))
+            continue;
+          const long long f = (long long)ly.R * ly.pitch;
+          if (f > pf) { pf = f; pick = l; }
+        }
+        if (pick < 0) break;
+        regmask |= 1u << pick;
+        regf += pf;
+      }
+      if (tv.n_reg > 0 && regmask == 0) continue;
+      for (unsigned m = 0; m <= all; m++) {
+        if (m & regmask) continue;
+        if (layout_smem(net, m, regmask, tv.rr * tv.rs * kThreads) > smem_cap) continue;
+        const long long f = resident_floats(d, m) + regf;
+        if (f > best) {
+          best = f;
+          mask = m;
+          net->reg_mask = regmask;
+          net->train_fn = tv.fn;
+          net->reg_tail = tv.rr * tv.rs * kThreads;
+          for (int k = 0; k < kMaxRegLayers; k++) d.reg_layer[k] = -1;
+          int k = 0;
+          for (int l = 0; l < H; l++)
+            if ((regmask >> l) & 1u) d.reg_layer[k++] = l;
+        }
+      }
     }
+  }
+  if (!net->train_fn) {
+    const TrainVariant* vars = nullptr;
+    train_variants(&vars);
+    net->train_fn = vars[0].fn;
+    for (int k = 0; k < kMaxRegLayers; k++) d.reg_layer[k] = -1;
   }
   if (layout_smem(net, 0) > smem_cap) {
     const int need = layout_smem(net, 0);
@@ -279,8 +330,10 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     return set_error(DMLP_EINVAL, "activation vectors need %d bytes of shared memory (> %d)",
                      need, smem_cap);
   }
-  net->residency = mask == all ? DMLP_RES_SMEM : (mask == 0 ? DMLP_RES_L2 : DMLP_RES_HYBRID);
-  net->smem_bytes = layout_smem(net, mask);
+  const unsigned onchip = mask | net->reg_mask;
+  net->residency =
+      onchip == all ? DMLP_RES_SMEM : (onchip == 0 ? DMLP_RES_L2 : DMLP_RES_HYBRID);
+  net->smem_bytes = layout_smem(net, mask, net->reg_mask, net->reg_tail);
   net->resident_mask = mask;
 
   int rc = DMLP_OK;
@@ -288,10 +341,12 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     dmlp_net_destroy(net);
     return code;
   };
-  if ((rc = cuda_check(set_train_attributes(net->smem_bytes), "cudaFuncSetAttribute")))
+  if ((rc = cuda_check(set_train_attributes(net->train_fn, net->smem_bytes),
+                       "cudaFuncSetAttribute")))
     return fail(rc);
   int bps = 0;
-  if ((rc = cuda_check(train_occupancy(net->smem_bytes, &bps), "occupancy"))) return fail(rc);
+  if ((rc = cuda_check(train_occupancy(net->train_fn, net->smem_bytes, &bps), "occupancy")))
+    return fail(rc);
   if (bps < 1)
     return fail(set_error(DMLP_ECUDA, "persistent kernel cannot be resident (%d smem bytes)",
                           net->smem_bytes));
@@ -360,6 +415,13 @@ int dmlp_net_info(dmlp_net* net, int32_t* residency, int32_t* n_ctas, int32_t* t
   return DMLP_OK;
 }
 
+int dmlp_net_layer_residency(dmlp_net* net, int32_t* where) {
+  if (!net || !where) return set_error(DMLP_EINVAL, "null argument");
+  for (int l = 0; l < net->dev.L; l++)
+    where[l] = (l == net->dev.L - 1) ? kResSmem : net->dev.ly[l].res;
+  return DMLP_OK;
+}
+
 int dmlp_net_profile(dmlp_net* net, int32_t enable) {
   if (!net) return set_error(DMLP_EINVAL, "null net");
   DMLP_CUDA(cudaSetDevice(net->device));
@@ -397,7 +459,7 @@ int dmlp_net_trace(dmlp_net* net, int64_t sample, uint64_t* marks /* [n_ctas][64
   return DMLP_OK;
 }
 
-int dmlp_net_read_profile(dmlp_net* net, int64_t* slots) {
+int dmlp_net_read_profile_all(dmlp_net* net, int64_t* slots, int32_t n_slots) {
   if (!net || !slots) return set_error(DMLP_EINVAL, "null argument");
   if (!net->dev.prof) return set_error(DMLP_EINVAL, "profiling is not enabled");
   DMLP_CUDA(cudaSetDevice(net->device));
@@ -410,14 +472,19 @@ int dmlp_net_read_profile(dmlp_net* net, int64_t* slots) {
     delete[] h;
     return cuda_check(e, "cudaMemcpy profile");
   }
-  for (int k = 0; k < kProfWords; k++) {
+  for (int k = 0; k < n_slots; k++) {
     long long a = 0;
-    for (int c = 0; c < net->dev.nct; c++) a += (long long)h[kProfWords * c + k];
+    if (k < kProfWords)
+      for (int c = 0; c < net->dev.nct; c++) a += (long long)h[kProfWords * c + k];
     slots[k] = a;
   }
   delete[] h;
   DMLP_CUDA(cudaMemset(net->dev.prof, 0, n * sizeof(unsigned long long)));
   return DMLP_OK;
+}
+
+int dmlp_net_read_profile(dmlp_net* net, int64_t* slots) {
+  return dmlp_net_read_profile_all(net, slots, kProfPhases);
 }
 
 int dmlp_net_set_layer(dmlp_net* net, int32_t layer, const float* w, int64_t n) {

@@ -13,7 +13,11 @@ constexpr int kThreads = 512;  // threads per CTA of the persistent kernel
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLayers = 16;
 constexpr int kMaxOut = 32;  // output layer: at most 32 classes
-constexpr int kProfWords = 16;  // profile slots per CTA
+constexpr int kProfPhases = 16;  // per-phase profile slots per CTA
+constexpr int kProfKinds = 5;    // per-layer slots: fwd, fwd gather, bwd partials, bwd update, bwd gather
+constexpr int kProfWords = kProfPhases + kProfKinds * 16;  // (kMaxLayers = 16)
+constexpr int kMaxRegLayers = 4;  // register-resident row blocks per CTA
+enum { kResL2 = 0, kResSmem = 1, kResReg = 2 };
 
 // One weight layer as the persistent kernel sees it.
 //
@@ -29,8 +33,8 @@ struct LayerDev {
   int fi, fo, pitch;     // fan-in, fan-out, floats per device row (>= fi+1, %4 == 0)
   int in_off;            // hidden l >= 1: smem offset of the gathered input vector (pitch long)
   int t_off;             // hidden: smem offset of the owned rows' tanh(B*a) cache
-  int res;               // hidden: 1 = the CTA's rows live in shared memory, 0 = streamed (L2)
-  int wsm_off;           // resident hidden rows / output tile: smem offset
+  int res;               // hidden: where the CTA's rows live: kResL2 / kResSmem / kResReg
+  int wsm_off;           // smem offset: resident hidden rows / register-block tail / output tile
   int R;                 // hidden: rows per CTA block; output: owned input columns per CTA
   int P;                 // CTAs owning at least one row (output: producing a partial)
   int gs, CH;            // hidden: log2 of the row groups G, rows per reduction chunk
@@ -54,6 +58,7 @@ struct NetDev {
   int red_off;   // [kWarps][32] reduction scratch
   int pbuf_off;  // [Gmax][pitch] per-row-group column partials (G > 1 layers)
   int out_off;   // output layer scratch: a | y | delta | eta*delta (kMaxOut each)
+  int reg_layer[kMaxRegLayers];  // register slot -> hidden layer (-1: unused)
   int* err;
   unsigned long long* prof;  // optional [nct][kProfWords] phase cycles (0 loop, 1 exchange)
   unsigned long long* trace;  // optional [nct][64] %globaltimer marks of one sample
@@ -82,6 +87,9 @@ struct dmlp_net {
   int* d_err = nullptr;
   int smem_bytes = 0;
   unsigned resident_mask = 0;
+  unsigned reg_mask = 0;
+  int reg_tail = 0;  // floats of shared-memory tail per register row block
+  const void* train_fn = nullptr;  // selected TrainVariant
   uint32_t seq = 1;  // next sample sequence number (flag value)
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;  // recorded after every operation on the net, whatever the stream
@@ -102,7 +110,14 @@ int net_end(dmlp_net* net, cudaStream_t st);
 cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
                          const uint8_t* labels, const int32_t* order, long long n, float eta,
                          uint32_t seq0, long long* wrong, float* y_last, cudaStream_t st);
-int train_smem_bytes(const dmlp_net* net);
-cudaError_t set_train_attributes(int smem_bytes);
-cudaError_t train_occupancy(int smem_bytes, int* blocks_per_sm);
+// Compiled instantiations of the training kernel: n_reg register row blocks
+// of at most rr rows x rc columns per thread (0 = none), plus rs column
+// slots per thread in shared memory.
+struct TrainVariant {
+  int n_reg, rr, rc, rs;  // rs: column slots of each block kept in a shared-memory tail
+  const void* fn;
+};
+int train_variants(const TrainVariant** out);
+cudaError_t set_train_attributes(const void* fn, int smem_bytes);
+cudaError_t train_occupancy(const void* fn, int smem_bytes, int* blocks_per_sm);
 }  // namespace dmlp

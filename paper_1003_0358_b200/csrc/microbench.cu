@@ -312,7 +312,54 @@ __global__ void __launch_bounds__(512, 1)
 
 using namespace dmlp;
 
+namespace dmlp {
+// Exhaustive check of the select-form tanhf against the branchy glibc
+// restatement, over every 32-bit pattern [start, start + count).
+__global__ void k_tanhf_check(unsigned long long start, unsigned long long count,
+                              unsigned long long* bad, unsigned int* first) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       i < count; i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t u = (uint32_t)(start + i);
+    const float x = u2f(u);
+    const uint32_t a = f2u(dev_tanhf(x)), b = f2u(dev_tanhf_branchy(x));
+    if (a != b && !((a & 0x7fffffffu) > 0x7f800000u && (b & 0x7fffffffu) > 0x7f800000u)) {
+      atomicAdd(bad, 1ull);
+      atomicMin(first, u);
+    }
+  }
+}
+__global__ void k_tanhf_eval(const float* x, float* y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = dev_tanhf(x[i]);
+}
+}  // namespace dmlp
+
 extern "C" {
+
+int dmlp_tanhf_check(uint64_t* mismatches, uint32_t* first_bad) {
+  unsigned long long* d = nullptr;
+  unsigned int* f = nullptr;
+  if (int rc = cuda_check(cudaMalloc(&d, 8), "cudaMalloc")) return rc;
+  if (int rc = cuda_check(cudaMalloc(&f, 4), "cudaMalloc")) return rc;
+  cudaMemset(d, 0, 8);
+  cudaMemset(f, 0xff, 4);
+  dmlp::k_tanhf_check<<<148 * 8, 256>>>(0ull, 1ull << 32, d, f);
+  if (int rc = cuda_check(cudaGetLastError(), "k_tanhf_check")) return rc;
+  if (int rc = cuda_check(cudaMemcpy(mismatches, d, 8, cudaMemcpyDeviceToHost), "cudaMemcpy"))
+    return rc;
+  if (int rc = cuda_check(cudaMemcpy(first_bad, f, 4, cudaMemcpyDeviceToHost), "cudaMemcpy"))
+    return rc;
+  cudaFree(d);
+  cudaFree(f);
+  return DMLP_OK;
+}
+
+int dmlp_tanhf_eval(const float* x_dev, float* y_dev, int64_t n) {
+  if (n <= 0) return DMLP_OK;
+  dmlp::k_tanhf_eval<<<148 * 4, 256>>>(x_dev, y_dev, n);
+  return cuda_check(cudaGetLastError(), "k_tanhf_eval");
+}
 
 int dmlp_bench(int32_t kind, int64_t bytes, int32_t iters, int32_t n_ctas, double* seconds,
                double* cycles) {

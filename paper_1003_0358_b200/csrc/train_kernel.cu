@@ -41,6 +41,7 @@
 namespace dmlp {
 
 constexpr int kProfSlots = kProfWords;
+template <int NRL, int RR, int RC, int RS>
 __global__ void __launch_bounds__(kThreads, 1)
     k_train(const NetDev net, const float* __restrict__ X, long long ldx,
             const uint8_t* __restrict__ labels, const int32_t* __restrict__ order,
@@ -56,6 +57,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const LayerDev& lo = net.ly[L - 1];
   const int OT = lo.R + 1;  // output tile row stride: owned columns + bias column
   float* otile = sm + lo.wsm_off;
+  float wr[NRL > 0 ? NRL : 1][RR][RC];  // register-resident row blocks (kResReg layers)
 
   if (tid < H) {
     const LayerDev& ly = net.ly[tid];
@@ -80,9 +82,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       v[i] = (i == net.ly[l].fi) ? 1.0f : 0.0f;
   }
   __syncthreads();
-  for (int l = 0; l < H; l++) {  // resident hidden layers: load the rows once
+#pragma unroll
+  for (int i = 0; i < NRL; i++) {  // register-resident row blocks
+    const int l = net.reg_layer[i];
+    const LayerDev& ly = net.ly[l < 0 ? 0 : l];
+    const int r0 = min(c * ly.R, ly.fo), nr = l < 0 ? 0 : min(ly.R, ly.fo - r0);
+    reg_load<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.w + (size_t)r0 * ly.pitch, ly.pitch, nr);
+  }
+  for (int l = 0; l < H; l++) {  // smem-resident hidden layers: load the rows once
     const LayerDev& ly = net.ly[l];
-    if (!ly.res) continue;
+    if (ly.res != kResSmem) continue;
     const float4* g = reinterpret_cast<const float4*>(ly.w + (size_t)g_r0[l] * ly.pitch);
     float4* s = reinterpret_cast<float4*>(sm + ly.wsm_off);
     for (int i = tid; i < g_nr[l] * ly.pitch / 4; i += kThreads) s[i] = g[i];
@@ -97,28 +106,42 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // Sample indices and labels are loaded ahead so no dependent global load
   // sits at the head of a sample.
-  long long img_cur = n > 0 ? (order ? order[0] : 0) : 0;
-  long long img_nxt = n > 1 ? (order ? order[1] : 1) : -1;
+  const int img_cur = n > 0 ? (order ? order[0] : 0) : 0;
+  int img_nxt = n > 1 ? (order ? order[1] : 1) : -1;
   int digit_cur = n > 0 ? labels[img_cur] : 0;
   if (n > 0) {
     for (int i = tid; i < net.ly[0].fi; i += kThreads)
-      cp_async4(sm + net.in0_off[0] + i, X + img_cur * ldx + i);
+      cp_async4(sm + net.in0_off[0] + i, X + (long long)img_cur * ldx + i);
     cp_async_commit();
   }
-  unsigned long long wrong = 0;  // counted by the last thread of CTA 0
+  __shared__ unsigned long long s_wrong;  // counted by the last thread of CTA 0
+  if (tid == 0) s_wrong = 0;
   const bool counter = (c == 0 && tid == kThreads - 1);
   // optional in-kernel profile (thread 0 of every CTA): per-phase cycles.
   // slot 0 loop total, 1 exchange waits; 2.. per phase (device.py names them).
   const bool prof = net.prof != nullptr && tid == 0;
   __shared__ long long ph[kProfSlots];  // per-phase cycles (thread 0 only)
-  if (tid < kProfSlots) ph[tid] = 0;
-  long long t_loop0 = prof ? clock64() : 0, t_xchg = 0, t_mark = 0;
-  long long t_ph = t_loop0;
+  for (int i = tid; i < kProfSlots; i += kThreads) ph[i] = 0;
+  // thread 0's clocks live in smem: no registers held across the loop
+  __shared__ long long pt[4];  // loop start, exchange total, exchange mark, phase mark
+  if (prof) pt[0] = pt[3] = clock64(), pt[1] = pt[2] = 0;
+#define t_loop0 pt[0]
+#define t_xchg pt[1]
+#define t_mark pt[2]
+#define t_ph pt[3]
 #define PH(slot)                    \
   if (prof) {                       \
     const long long _t = clock64(); \
     ph[slot] += _t - t_ph;          \
     t_ph = _t;                      \
+  }
+  // PHL: the same, also booked to layer `ly_` under per-layer kind `k_`.
+#define PHL(slot, ly_, k_)                                   \
+  if (prof) {                                                \
+    const long long _t = clock64();                          \
+    ph[slot] += _t - t_ph;                                   \
+    ph[kProfPhases + kProfKinds * (ly_) + (k_)] += _t - t_ph; \
+    t_ph = _t;                                               \
   }
 #define XB() \
   if (prof) t_mark = clock64();
@@ -138,10 +161,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }                                                                         \
   }
 
-  for (long long s = 0; s < n; s++) {
+  for (int s = 0; s < n; s++) {
     const uint32_t seq = seq0 + (uint32_t)s;
     const int buf = seq & 1;
-    const long long img_nn = (s + 2 < n) ? (order ? order[s + 2] : s + 2) : -1;
+    const int img_nn = (s + 2 < n) ? (order ? order[s + 2] : s + 2) : -1;
     const int digit = digit_cur;
     const int digit_nxt = img_nxt >= 0 ? labels[img_nxt] : 0;
     float* in0 = sm + net.in0_off[s & 1];
@@ -152,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (img_nxt >= 0) {  // prefetch the next sample's input under this sample
       float* nx = sm + net.in0_off[(s + 1) & 1];
       for (int i = tid; i < net.ly[0].fi; i += kThreads)
-        cp_async4(nx + i, X + img_nxt * ldx + i);
+        cp_async4(nx + i, X + (long long)img_nxt * ldx + i);
       cp_async_commit();
     }
 
@@ -167,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            net.err);
         __syncthreads();
         XE();
-        PH(4);
+        PHL(4, l, 1);
         TRACE(2 + 2 * (l - 1));
       }
       if (mine) {
@@ -176,14 +199,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             (l < H - 1) ? ly.yll + ((size_t)buf * ly.P << ly.ylog) + ((size_t)c << ly.ylog)
                         : nullptr;
         float* yo = (l == H - 1) ? sm + net.yown_off : nullptr;
-        if (ly.res)
+        if (ly.res == kResReg) {
+#pragma unroll
+          for (int i = 0; i < NRL; i++)
+            if (net.reg_layer[i] == l)
+              reg_fwd<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.pitch, g_nr[l],
+                                  reinterpret_cast<const float*>(v4), red, sm + ly.t_off, yo,
+                                  ys, seq);
+        } else if (ly.res == kResSmem)
           fwd_dispatch<true>(reinterpret_cast<const float4*>(sm + ly.wsm_off), ly, g_nr[l], v4,
-                             red, sm + ly.t_off, yo, ys, seq);
+                             red, sm + ly.t_off, yo, ys, seq, prof ? ph + 12 : nullptr);
         else
           fwd_dispatch<false>(reinterpret_cast<const float4*>(ly.w + (size_t)g_r0[l] * ly.pitch),
                               ly, g_nr[l], v4, red, sm + ly.t_off, yo, ys, seq);
       }
-      PH(3);
+      PHL(3, l, 0);
       if (l < H - 1) TRACE(1 + 2 * l);
     }
 
@@ -213,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float a = outv[tid];
         float t;
         const float y = tanh_scaled_noinline(a, &t);
-        const float d = dev_output_delta(y, a, tid == digit ? 1.0f : -1.0f);
+        const float d = dev_output_delta_t(y, t, tid == digit ? 1.0f : -1.0f);
         outv[kMaxOut + tid] = y;
         outv[2 * kMaxOut + tid] = d;
         outv[3 * kMaxOut + tid] = __fmul_rn(eta, d);
@@ -226,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float yk = outv[kMaxOut + k];
           if (yk > bv || yk != yk) { bv = yk; best = k; }
         }
-        wrong += (best != digit);
+        s_wrong += (best != digit);
       }
       if (c == 0 && s == n - 1 && y_last != nullptr && tid < lo.fo)
         y_last[tid] = outv[kMaxOut + tid];
@@ -270,7 +300,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (mine) {
         unsigned long long* ps = pb + (size_t)c * ly.pstride;
         const float4* v4 = reinterpret_cast<const float4*>(sm + ly.in_off);
-        if (ly.res)
+        if (ly.res == kResReg) {
+#pragma unroll
+          for (int i = 0; i < NRL; i++)
+            if (net.reg_layer[i] == l)
+              reg_partials<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.fi, g_nr[l], dl, ps, seq);
+        } else if (ly.res == kResSmem)
           bwd_partials<true, false>(reinterpret_cast<float4*>(sm + ly.wsm_off), ly.pitch >> 2,
                                     ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
         else
@@ -278,12 +313,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               reinterpret_cast<float4*>(ly.w + (size_t)g_r0[l] * ly.pitch), ly.pitch >> 2,
               ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
       }
-      PH(8);
+      PHL(8, l, 2);
       TRACE(1 + 2 * (L - 1 + (H - 1 - l)));
-      if (mine && ly.res)
+      if (mine && ly.res == kResSmem)
         update_rows<true>(reinterpret_cast<float4*>(sm + ly.wsm_off), ly.pitch >> 2, ly.gs,
                           g_nr[l], reinterpret_cast<const float4*>(sm + ly.in_off), sl);
-      PH(9);
+      if (mine && ly.res == kResReg) {
+#pragma unroll
+        for (int i = 0; i < NRL; i++)
+          if (net.reg_layer[i] == l)
+            reg_update<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.pitch, g_nr[l], sm + ly.in_off,
+                                   sl);
+      }
+      PHL(9, l, 3);
       const int nxt = cur ^ 1;
       const LayerDev& lb = net.ly[l - 1];
       float* dn = sm + net.delta_off[nxt];
@@ -300,14 +342,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       else
         __syncthreads();
       XE();
-      PH(10);
+      PHL(10, l, 4);
       TRACE(2 + 2 * (L - 1 + (H - 1 - l)));
       cur = nxt;
     }
     if (H > 0 && c < net.ly[0].P) {
       const LayerDev& l0 = net.ly[0];
       const float4* x4 = reinterpret_cast<const float4*>(in0);
-      if (l0.res)
+      if (l0.res == kResReg) {
+#pragma unroll
+        for (int i = 0; i < NRL; i++)
+          if (net.reg_layer[i] == 0)
+            reg_update<RR, RC, RS>(wr[i], sm + l0.wsm_off, l0.pitch, g_nr[0], in0,
+                                   sm + net.dsc_off[cur]);
+      } else if (l0.res == kResSmem)
         update_rows<true>(reinterpret_cast<float4*>(sm + l0.wsm_off), l0.pitch >> 2, l0.gs,
                           g_nr[0], x4, sm + net.dsc_off[cur]);
       else
@@ -316,15 +364,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     PH(11);
     TRACE(63);
-    img_cur = img_nxt;
     img_nxt = img_nn;
     digit_cur = digit_nxt;
   }
   __syncthreads();
 
+#pragma unroll
+  for (int i = 0; i < NRL; i++) {
+    const int l = net.reg_layer[i];
+    if (l < 0) continue;
+    const LayerDev& ly = net.ly[l];
+    const int r0 = min(c * ly.R, ly.fo), nr = min(ly.R, ly.fo - r0);
+    reg_store<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.w + (size_t)r0 * ly.pitch, ly.pitch, nr);
+  }
   for (int l = 0; l < H; l++) {  // write the resident rows back
     const LayerDev& ly = net.ly[l];
-    if (!ly.res) continue;
+    if (ly.res != kResSmem) continue;
     float4* g = reinterpret_cast<float4*>(ly.w + (size_t)g_r0[l] * ly.pitch);
     const float4* s = reinterpret_cast<const float4*>(sm + ly.wsm_off);
     for (int i = tid; i < g_nr[l] * ly.pitch / 4; i += kThreads) g[i] = s[i];
@@ -341,19 +396,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       atomicAdd(net.prof + kProfSlots * c + k, (unsigned long long)ph[k]);
   }
 #undef PH
+#undef t_loop0
+#undef t_xchg
+#undef t_mark
+#undef t_ph
+#undef PHL
 #undef XB
 #undef XE
 #undef TRACE
-  if (counter && wrong_out != nullptr) atomicAdd(wrong_out, wrong);
+  if (counter && wrong_out != nullptr) atomicAdd(wrong_out, s_wrong);
 }
 
-cudaError_t set_train_attributes(int smem_bytes) {
-  return cudaFuncSetAttribute(k_train, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+// The compiled register plans: none; one 14-row block of 4 register column
+// slots + 1 shared-memory slot (the 2000x2501 hidden layer of C4: 14 rows x
+// 2504 columns per CTA); and up to four 7-row x 2-column blocks (1000-wide
+// layers: C5).
+static const TrainVariant kVariants[] = {
+    {0, 1, 1, 0, (const void*)k_train<0, 1, 1, 0>},
+    {1, 14, 4, 1, (const void*)k_train<1, 14, 4, 1>},
+    {2, 7, 2, 0, (const void*)k_train<2, 7, 2, 0>},
+    {4, 7, 2, 0, (const void*)k_train<4, 7, 2, 0>},
+};
+
+int train_variants(const TrainVariant** out) {
+  *out = kVariants;
+  return (int)(sizeof(kVariants) / sizeof(kVariants[0]));
 }
 
-cudaError_t train_occupancy(int smem_bytes, int* blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_train, kThreads,
-                                                       smem_bytes);
+cudaError_t set_train_attributes(const void* fn, int smem_bytes) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+}
+
+cudaError_t train_occupancy(const void* fn, int smem_bytes, int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads, smem_bytes);
 }
 
 cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
@@ -362,7 +437,7 @@ cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
   NetDev nd = net->dev;
   unsigned long long* w = reinterpret_cast<unsigned long long*>(wrong);
   void* args[] = {&nd, &x, &ldx, &labels, &order, &n, &eta, &seq0, &w, &y_last};
-  return cudaLaunchCooperativeKernel((const void*)k_train, dim3(nd.nct), dim3(kThreads), args,
+  return cudaLaunchCooperativeKernel(net->train_fn, dim3(nd.nct), dim3(kThreads), args,
                                      (size_t)net->smem_bytes, st);
 }
 

@@ -26,7 +26,7 @@ __device__ __noinline__ void spin_fail(int* err) {
   atomicExch(err, 1);
   __trap();
 }
-__device__ __noinline__ float tanh_scaled_noinline(float a, float* t) {
+__device__ __forceinline__ float tanh_scaled_noinline(float a, float* t) {
   return dev_scaled_tanh(a, t);
 }
 
@@ -108,6 +108,21 @@ struct RowMap {
 };
 static_assert(kThreads == 512, "RowMap assumes 512 threads");
 
+// Sum of n (a power of two <= 16) values r[0], r[S], r[2S], ...: every load
+// issued at once, then a fixed pairwise tree -- deterministic, and no serial
+// load-add chain on the critical path.
+template <int S>
+__device__ __forceinline__ float tree_sum(const float* r, int n) {
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) v[i] = i < n ? r[i * S] : 0.0f;
+#pragma unroll
+  for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+    for (int i = 0; i < h; i++) v[i] += v[i + h];
+  return v[0];
+}
+
 // Forward of the owned rows [0, nr) of a hidden layer.  Per-thread partial
 // rows over its quads, a transposing warp reduction, a fixed-order sum over
 // the group's warps; one thread per row then applies the scaled tanh, caches
@@ -115,7 +130,15 @@ static_assert(kThreads == 512, "RowMap assumes 512 threads");
 template <bool RES, int CH>
 __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, int gs, int nr,
                                          const float4* __restrict__ v4, float* red, float* tc,
-                                         float* yown, unsigned long long* yslot, uint32_t seq) {
+                                         float* yown, unsigned long long* yslot, uint32_t seq,
+                                         long long* sub = nullptr) {
+  long long t0 = sub ? clock64() : 0;
+#define SUBP(i)                     \
+  if (sub) {                        \
+    const long long _t = clock64(); \
+    sub[i] += _t - t0;              \
+    t0 = _t;                        \
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const RowMap mp(gs, nr);
   const int G = 1 << gs, WG = kWarps >> gs;
@@ -129,20 +152,33 @@ __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, 
     const float4* Wg = W4 + (mp.g + (j0 << gs)) * nq;
     for (int q = mp.u; q < nq; q += mp.TG) {
       const float4 x = v4[q];
+      // rows in groups of FB loads: the empty asm keeps the compiler from
+      // hoisting every load of the chunk (register budget)
+      constexpr int FB = RES ? 4 : 8;
 #pragma unroll
-      for (int jj = 0; jj < CH; jj++)
-        if (jj < jn) acc[jj] = dot4(ldw4<RES>(Wg + jj * rstep + q), x, acc[jj]);
+      for (int j4 = 0; j4 < CH; j4 += FB) {
+        float4 w[FB];
+#pragma unroll
+        for (int i = 0; i < FB; i++)
+          w[i] = (j4 + i < CH && j4 + i < jn) ? ldw4<RES>(Wg + (j4 + i) * rstep + q)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < FB; i++)
+          if (j4 + i < CH) acc[j4 + i < CH ? j4 + i : 0] = dot4(w[i], x, acc[j4 + i < CH ? j4 + i : 0]);
+        asm volatile("" ::: "memory");
+      }
     }
     const float s = xpose_reduce<CH>(acc, lane);
     if ((lane & (32 / CH - 1)) == 0) red[warp * CH + lane / (32 / CH)] = s;
+    SUBP(0);
     __syncthreads();
+    SUBP(1);
     if (tid < G * CH) {
       const int gg = tid / CH, jj = tid - gg * CH;
       const int k = gg + G * (j0 + jj);
       if (k < nr) {
-        const float* r = red + gg * WG * CH + jj;
-        float a = r[0];
-        for (int w = 1; w < WG; w++) a += r[w * CH];
+        const float a = tree_sum<CH>(red + gg * WG * CH + jj, WG);
+        SUBP(2);
         float t;
         const float y = tanh_scaled_noinline(a, &t);
         tc[k] = t;
@@ -150,20 +186,22 @@ __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, 
         if (yslot) st_flag(yslot + k, y, seq);
       }
     }
+    SUBP(3);
     if (j0 + CH < njmax) __syncthreads();  // red is reused by the next chunk
   }
+#undef SUBP
 }
 
 template <bool RES>
 __device__ __forceinline__ void fwd_dispatch(const float4* W4, const LayerDev& ly, int nr,
                                              const float4* v4, float* red, float* tc,
                                              float* yown, unsigned long long* yslot,
-                                             uint32_t seq) {
+                                             uint32_t seq, long long* sub = nullptr) {
   const int nq = ly.pitch >> 2, gs = ly.gs;
   switch (ly.CH) {
-    case 4: fwd_rows<RES, 4>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq); break;
-    case 8: fwd_rows<RES, 8>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq); break;
-    default: fwd_rows<RES, 16>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq); break;
+    case 4: fwd_rows<RES, 4>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
+    case 8: fwd_rows<RES, 8>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
+    default: fwd_rows<RES, 16>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
   }
 }
 
@@ -251,25 +289,151 @@ __device__ __forceinline__ void update_rows(float4* W4, int nq, int gs, int nr,
   }
 }
 
+// ---- register-resident row blocks -------------------------------------------
+// A hidden layer whose owned rows do not fit in shared memory can live in the
+// register file (256 KB per SM): thread t holds column t + 512*m (m < RC) of
+// every owned row k < RR, zeros beyond the layer's rows and columns.  RS more
+// column slots m = RC .. RC+RS-1 of the same mapping live in a shared-memory
+// tail [RS][RR][512] (conflict-free: consecutive threads, consecutive words),
+// so a layer slightly too wide for the register budget still avoids L2.  Its
+// forward, column partials and update are then FMA work on registers; only
+// the tail, the input vector and the deltas are read from shared memory.
+
+template <int RR, int RS>
+__device__ __forceinline__ float& tail_at(float* tail, int m, int k) {
+  return tail[(m * RR + k) * kThreads + threadIdx.x];
+}
+
+template <int RR, int RC, int RS>
+__device__ __forceinline__ void reg_load(float (&w)[RR][RC], float* tail,
+                                         const float* __restrict__ g, int pitch, int nr) {
+#pragma unroll
+  for (int k = 0; k < RR; k++) {
+#pragma unroll
+    for (int m = 0; m < RC; m++) {
+      const int c = threadIdx.x + kThreads * m;
+      w[k][m] = (k < nr && c < pitch) ? g[k * pitch + c] : 0.0f;
+    }
+#pragma unroll
+    for (int m = 0; m < RS; m++) {
+      const int c = threadIdx.x + kThreads * (RC + m);
+      tail_at<RR, RS>(tail, m, k) = (k < nr && c < pitch) ? g[k * pitch + c] : 0.0f;
+    }
+  }
+}
+
+template <int RR, int RC, int RS>
+__device__ __forceinline__ void reg_store(const float (&w)[RR][RC], float* tail, float* g,
+                                          int pitch, int nr) {
+#pragma unroll
+  for (int k = 0; k < RR; k++) {
+#pragma unroll
+    for (int m = 0; m < RC; m++) {
+      const int c = threadIdx.x + kThreads * m;
+      if (k < nr && c < pitch) g[k * pitch + c] = w[k][m];
+    }
+#pragma unroll
+    for (int m = 0; m < RS; m++) {
+      const int c = threadIdx.x + kThreads * (RC + m);
+      if (k < nr && c < pitch) g[k * pitch + c] = tail_at<RR, RS>(tail, m, k);
+    }
+  }
+}
+
+template <int RR, int RC, int RS>
+__device__ __forceinline__ void reg_fwd(const float (&w)[RR][RC], float* tail, int pitch, int nr,
+                                        const float* __restrict__ v, float* red, float* tc,
+                                        float* yown, unsigned long long* yslot, uint32_t seq) {
+  static_assert(RR <= 16, "register row block: at most 16 rows");
+  constexpr int CH = RR <= 4 ? 4 : RR <= 8 ? 8 : 16;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float acc[CH];
+#pragma unroll
+  for (int k = 0; k < CH; k++) acc[k] = 0.0f;
+#pragma unroll
+  for (int m = 0; m < RC; m++) {
+    const int c = tid + kThreads * m;
+    const float x = c < pitch ? v[c] : 0.0f;
+#pragma unroll
+    for (int k = 0; k < RR; k++) acc[k] = fmaf(w[k][m], x, acc[k]);
+  }
+#pragma unroll
+  for (int m = 0; m < RS; m++) {
+    const int c = tid + kThreads * (RC + m);
+    const float x = c < pitch ? v[c] : 0.0f;
+#pragma unroll
+    for (int k = 0; k < RR; k++) acc[k] = fmaf(tail_at<RR, RS>(tail, m, k), x, acc[k]);
+  }
+  const float s = xpose_reduce<CH>(acc, lane);
+  if ((lane & (32 / CH - 1)) == 0) red[warp * CH + lane / (32 / CH)] = s;
+  __syncthreads();
+  if (tid < nr) {
+    const float a = tree_sum<CH>(red + tid, kWarps);
+    float t;
+    const float y = tanh_scaled_noinline(a, &t);
+    tc[tid] = t;
+    if (yown) yown[tid] = y;
+    if (yslot) st_flag(yslot + tid, y, seq);
+  }
+}
+
+template <int RR, int RC, int RS>
+__device__ __forceinline__ void reg_partials(const float (&w)[RR][RC], float* tail, int fi,
+                                             int nr, const float* __restrict__ delta,
+                                             unsigned long long* pslot, uint32_t seq) {
+  float d[RR];
+#pragma unroll
+  for (int k = 0; k < RR; k++) d[k] = k < nr ? delta[k] : 0.0f;
+#pragma unroll
+  for (int m = 0; m < RC + RS; m++) {
+    const int c = threadIdx.x + kThreads * m;
+    float p = 0.0f;
+#pragma unroll
+    for (int k = 0; k < RR; k++)
+      p = fmaf(m < RC ? w[k][m < RC ? m : 0] : tail_at<RR, RS>(tail, m - RC, k), d[k], p);
+    if (c < fi) st_flag(pslot + c, p, seq);
+  }
+}
+
+template <int RR, int RC, int RS>
+__device__ __forceinline__ void reg_update(float (&w)[RR][RC], float* tail, int pitch, int nr,
+                                           const float* __restrict__ v,
+                                           const float* __restrict__ dsc) {
+#pragma unroll
+  for (int m = 0; m < RC + RS; m++) {
+    const int c = threadIdx.x + kThreads * m;
+    const float x = c < pitch ? v[c] : 0.0f;
+#pragma unroll
+    for (int k = 0; k < RR; k++) {
+      const float sk = k < nr ? dsc[k] : 0.0f;
+      if (m < RC) w[k][m < RC ? m : 0] = upd(w[k][m < RC ? m : 0], sk, x);
+      else tail_at<RR, RS>(tail, m - RC, k) = upd(tail_at<RR, RS>(tail, m - RC, k), sk, x);
+    }
+  }
+}
+
 // Poll a batch of U flag words per thread in rounds: every round re-issues
 // the loads of all words not ready yet, so a late producer costs one L2
-// round trip per round, not one per word.
+// round trip per round, not one per word.  Word u is base[off[u]]
+// (off < 0: none); 32-bit offsets keep the register footprint small.
 template <int U>
-__device__ __forceinline__ void poll_batch(const unsigned long long* const (&ptr)[U],
+__device__ __forceinline__ void poll_batch(const unsigned long long* base, const int (&off)[U],
                                            unsigned long long (&v)[U], uint32_t seq,
                                            int* err) {
+#pragma unroll
+  for (int u = 0; u < U; u++) v[u] = off[u] >= 0 ? ld_flag(base + off[u]) : 0ull;
   long long t0 = 0;
   for (int round = 0;; round++) {
     bool done = true;
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (ptr[u] != nullptr && (uint32_t)(v[u] >> 32) != seq) done = false;
+      if (off[u] >= 0 && (uint32_t)(v[u] >> 32) != seq) done = false;
     if (done) return;
     if (round == 0) t0 = clock64();
     else if (clock64() - t0 > kSpinTimeoutCycles) spin_fail(err);
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (ptr[u] != nullptr && (uint32_t)(v[u] >> 32) != seq) v[u] = ld_flag(ptr[u]);
+      if (off[u] >= 0 && (uint32_t)(v[u] >> 32) != seq) v[u] = ld_flag(base + off[u]);
   }
 }
 
@@ -285,7 +449,7 @@ __device__ __forceinline__ void gather_y(const unsigned long long* src, const La
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nseg = (ly.R + 31) >> 5, V = ly.P * nseg;
   for (int vb = 0; vb < V; vb += kWarps * kGatherU) {
-    const unsigned long long* ptr[kGatherU];
+    int off[kGatherU];
     unsigned long long v[kGatherU];
 #pragma unroll
     for (int u = 0; u < kGatherU; u++) {
@@ -293,27 +457,24 @@ __device__ __forceinline__ void gather_y(const unsigned long long* src, const La
       const int p = nseg == 1 ? vi : vi / nseg;
       const int k = (vi - p * nseg) * 32 + lane;
       const bool ok = vi < V && k < ly.R && p * ly.R + k < ly.fo;
-      ptr[u] = ok ? src + ((size_t)p << ly.ylog) + k : nullptr;
-      v[u] = ok ? ld_flag(ptr[u]) : 0ull;
+      off[u] = ok ? (p << ly.ylog) + k : -1;
     }
-    poll_batch<kGatherU>(ptr, v, seq, err);
+    poll_batch<kGatherU>(src, off, v, seq, err);
+    const int kmask = (1 << ly.ylog) - 1;
 #pragma unroll
-    for (int u = 0; u < kGatherU; u++)
-      if (ptr[u] != nullptr) {
-        const int vi = vb + warp + kWarps * u;
-        const int p = nseg == 1 ? vi : vi / nseg;
-        dst[p * ly.R + (vi - p * nseg) * 32 + lane] = __uint_as_float((uint32_t)v[u]);
-      }
+    for (int u = 0; u < kGatherU; u++)  // slot offset -> row: p * R + k
+      if (off[u] >= 0)
+        dst[(off[u] >> ly.ylog) * ly.R + (off[u] & kmask)] = __uint_as_float((uint32_t)v[u]);
   }
 }
 
-// s_k = sum over producers c < P of src[c*stride + off + k], k < nr, in a
+// s_k = sum over producers c < P of src[c*stride + o + k], k < nr, in a
 // fixed order (producers c = w + 16*i summed by warp w in ascending i, then
 // the 16 warp sums in ascending w): deterministic, independent of timing,
 // no staging buffer.  fin(k, s_k) runs on one thread per k.
 template <class Fin>
 __device__ __forceinline__ void gather_sum(const unsigned long long* src, int stride, int P,
-                                           int off, int nr, float* red, uint32_t seq, int* err,
+                                           int o, int nr, float* red, uint32_t seq, int* err,
                                            Fin fin) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int k0 = 0; k0 < nr; k0 += 32) {
@@ -321,26 +482,22 @@ __device__ __forceinline__ void gather_sum(const unsigned long long* src, int st
     const bool kv = k < nr;
     float acc = 0.0f;
     for (int pb = 0; pb < P; pb += kWarps * kGatherU) {
-      const unsigned long long* ptr[kGatherU];
+      int off[kGatherU];
       unsigned long long v[kGatherU];
 #pragma unroll
       for (int u = 0; u < kGatherU; u++) {
         const int p = pb + warp + kWarps * u;
-        const bool ok = kv && p < P;
-        ptr[u] = ok ? src + (size_t)p * stride + off + k : nullptr;
-        v[u] = ok ? ld_flag(ptr[u]) : 0ull;
+        off[u] = (kv && p < P) ? p * stride + o + k : -1;
       }
-      poll_batch<kGatherU>(ptr, v, seq, err);
+      poll_batch<kGatherU>(src, off, v, seq, err);
 #pragma unroll
       for (int u = 0; u < kGatherU; u++)
-        if (ptr[u] != nullptr) acc += __uint_as_float((uint32_t)v[u]);
+        if (off[u] >= 0) acc += __uint_as_float((uint32_t)v[u]);
     }
     red[warp * 32 + lane] = acc;
     __syncthreads();
     if (tid < 32 && k0 + tid < nr) {
-      float s = red[tid];
-      for (int w = 1; w < kWarps; w++) s += red[w * 32 + tid];
-      fin(k0 + tid, s);
+      fin(k0 + tid, tree_sum<32>(red + tid, kWarps));
     }
     __syncthreads();
   }

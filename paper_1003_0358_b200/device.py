@@ -45,7 +45,7 @@ class DeviceNet:
         if isinstance(residency, int):  # explicit resident-layer bitmask
             code = 0x10000 | residency
         else:
-            code = _lib.RESIDENCY[residency]
+            code = (_lib.RES_AUTO | 0x20000) if residency == "auto-noreg" else _lib.RESIDENCY[residency]
         _lib.check(_lib.lib().dmlp_net_create(self.device, sizes, len(self.layer_sizes), code,
                                               int(n_ctas), ctypes.byref(h)), "dmlp_net_create")
         self._h = h
@@ -54,6 +54,11 @@ class DeviceNet:
                                             ctypes.byref(t), ctypes.byref(s)), "dmlp_net_info")
         self.residency = {v: k for k, v in _lib.RESIDENCY.items()}[r.value]
         self.n_ctas, self.threads, self.smem_bytes = c.value, t.value, s.value
+        where = (ctypes.c_int32 * len(self.layer_sizes))()
+        _lib.check(_lib.lib().dmlp_net_layer_residency(self._h, where), "dmlp_net_layer_residency")
+        #: per weight layer: "l2" (streamed every sample), "smem" or "reg" (register file)
+        self.layer_residency = [("l2", "smem", "reg")[where[i]]
+                                for i in range(len(self.layer_sizes) - 1)]
 
     # -- lifetime ---------------------------------------------------------------
     def close(self):
@@ -105,13 +110,21 @@ class DeviceNet:
                      "out_stage", "bwd_part", "bwd_upd", "bwd_xchg", "upd0", "s12", "s13", "s14",
                      "s15")
 
+    LAYER_KINDS = ("fwd", "fwd_gather", "bwd_part", "bwd_upd", "bwd_gather")
+
     def read_profile(self) -> dict:
         """Per-phase cycles summed over CTAs since the last read (thread 0's
-        view), plus the exchange ("grid-sync stall") fraction."""
-        buf = (ctypes.c_int64 * 16)()
-        _lib.check(_lib.lib().dmlp_net_read_profile(self._h, buf), "dmlp_net_read_profile")
+        view), the exchange ("grid-sync stall") fraction, and under "layers"
+        the per-layer split (LAYER_KINDS) of the layer phases."""
+        n = 16 + 5 * 16
+        buf = (ctypes.c_int64 * n)()
+        _lib.check(_lib.lib().dmlp_net_read_profile_all(self._h, buf, n),
+                   "dmlp_net_read_profile_all")
         d = {k: buf[i] for i, k in enumerate(self.PROFILE_SLOTS)}
         d["exchange_fraction"] = (d["exchange"] / d["loop"]) if d["loop"] else 0.0
+        L = len(self.layer_sizes) - 1
+        d["layers"] = [{k: buf[16 + 5 * l + j] for j, k in enumerate(self.LAYER_KINDS)}
+                       for l in range(L)]
         return d
 
     def trace(self, sample: int = -1):

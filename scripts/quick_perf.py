@@ -33,7 +33,7 @@ for name in names:
     pr = dn.read_profile() if prof else {}
     W = sum((i + 1) * o for i, o in zip(sizes[:-1], sizes[1:]))
     sps = n / (ms / 1e3)
-    print(json.dumps({"cfg": name, "res": dn.residency, "nct": dn.n_ctas, "smem": dn.smem_bytes,
+    print(json.dumps({"cfg": name, "res": dn.residency, "where": "".join(w[0] for w in dn.layer_residency), "nct": dn.n_ctas, "smem": dn.smem_bytes,
                       "us_per_sample": round(ms * 1e3 / n, 3), "samples_s": round(sps),
-                      "GBs_12B": round(12 * W * sps / 1e9, 1), **({"xchg_frac": round(pr["exchange_fraction"], 3), "phases_per_sample": {k: v // dn.n_ctas // n for k, v in pr.items() if k not in ("exchange_fraction",) and v}} if prof else {})}))
+                      "GBs_12B": round(12 * W * sps / 1e9, 1), **({"xchg_frac": round(pr["exchange_fraction"], 3), "phases_per_sample": {k: v // dn.n_ctas // n for k, v in pr.items() if k not in ("exchange_fraction", "layers") and v}, "per_layer": [[v // dn.n_ctas // n for v in lay.values()] for lay in pr["layers"]]} if prof else {})}))
     dn.close()

@@ -144,3 +144,64 @@ def test_errors_map_to_reference_exceptions():
         dn.train_step(np.zeros(840, np.float32), 1, 1e-3)
     with pytest.raises(ValueError):
         dn.train_step(np.zeros(841, np.float32), 1, -1.0)
+
+
+def test_device_tanhf_select_form_exhaustive():
+    """The kernel's select-form tanhf equals the branchy glibc restatement on
+    all 2^32 inputs (NaN payloads aside)."""
+    import ctypes
+
+    from paper_1003_0358_b200 import _lib
+
+    bad, first = ctypes.c_uint64(), ctypes.c_uint32()
+    _lib.check(_lib.lib().dmlp_tanhf_check(ctypes.byref(bad), ctypes.byref(first)),
+               "dmlp_tanhf_check")
+    assert bad.value == 0, hex(first.value)
+
+
+def test_device_tanhf_matches_libm():
+    """Device tanhf vs the host glibc tanhf (the oracle's libm call) on a
+    random sample of bit patterns plus the edge values."""
+    import torch
+
+    from paper_1003_0358_b200 import _lib
+
+    rng = np.random.default_rng(5)
+    bits = rng.integers(0, 2**32, size=20000, dtype=np.uint64).astype(np.uint32)
+    x = np.concatenate([bits.view(np.float32),
+                        np.array([0.0, -0.0, 1.0, -1.0, 22.0, -22.0, 1e-30, 0.34657, 9.5,
+                                  np.inf, -np.inf, 1e-8, 88.0], np.float32),
+                        rng.normal(0, 1.5, 20000).astype(np.float32)])
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    _lib.check(_lib.lib().dmlp_tanhf_eval(xd.data_ptr(), yd.data_ptr(), x.size), "tanhf_eval")
+    y = yd.cpu().numpy()
+    L = O.lib()
+    ref = np.array([L.or_tanhf(float(v)) for v in x], np.float32)
+    same = (y.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(y) & np.isnan(ref))
+    assert same.all(), x[~same][:5]
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_train_epoch_headline_configs(golden, cfg):
+    """The BASELINE configs with their auto residency (register row blocks,
+    shared memory and streamed layers): 160 on-line samples in one launch vs
+    the oracle's epoch on identical inputs."""
+    import torch
+
+    sizes = {"C4": (841, 2500, 2000, 1500, 1000, 500, 10),
+             "C5": (841,) + (1000,) * 9 + (10,)}[cfg]
+    g = golden("train")
+    x, lab = _inputs(golden)
+    n = 160
+    order = (np.arange(n) * 37) % 64
+    ref = O.init_layers(0, sizes)
+    dn = _net(sizes, [w.copy() for w in ref])
+    O.set_threads(8)
+    wrong_ref = O.train_epoch(ref, g["deformed"], lab, 1e-3, order=order)
+    wrong = torch.zeros((), dtype=torch.int64, device="cuda")
+    dn.train_epoch(torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda(),
+                   torch.from_numpy(order.astype(np.int32)).cuda(), 1e-3, wrong)
+    torch.cuda.synchronize()
+    assert int(wrong.item()) == wrong_ref
+    _assert_weights_close(dn.get_layers(), ref)
