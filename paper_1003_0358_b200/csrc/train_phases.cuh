@@ -170,17 +170,17 @@ __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, 
     }
     const float s = xpose_reduce<CH>(acc, lane);
     if ((lane & (32 / CH - 1)) == 0) red[warp * CH + lane / (32 / CH)] = s;
-    SUBP(0);
     __syncthreads();
-    SUBP(1);
+    SUBP(0);
     if (tid < G * CH) {
       const int gg = tid / CH, jj = tid - gg * CH;
       const int k = gg + G * (j0 + jj);
       if (k < nr) {
         const float a = tree_sum<CH>(red + gg * WG * CH + jj, WG);
-        SUBP(2);
+        SUBP(1);
         float t;
         const float y = tanh_scaled_noinline(a, &t);
+        SUBP(2);
         tc[k] = t;
         if (yown) yown[k] = y;
         if (yslot) st_flag(yslot + k, y, seq);
@@ -416,6 +416,9 @@ __device__ __forceinline__ void reg_update(float (&w)[RR][RC], float* tail, int 
 // the loads of all words not ready yet, so a late producer costs one L2
 // round trip per round, not one per word.  Word u is base[off[u]]
 // (off < 0: none); 32-bit offsets keep the register footprint small.
+#ifndef DMLP_POLL_BACKOFF_NS
+#define DMLP_POLL_BACKOFF_NS 0
+#endif
 template <int U>
 __device__ __forceinline__ void poll_batch(const unsigned long long* base, const int (&off)[U],
                                            unsigned long long (&v)[U], uint32_t seq,
@@ -431,6 +434,7 @@ __device__ __forceinline__ void poll_batch(const unsigned long long* base, const
     if (done) return;
     if (round == 0) t0 = clock64();
     else if (clock64() - t0 > kSpinTimeoutCycles) spin_fail(err);
+    if (DMLP_POLL_BACKOFF_NS > 0) __nanosleep(DMLP_POLL_BACKOFF_NS);
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (off[u] >= 0 && (uint32_t)(v[u] >> 32) != seq) v[u] = ld_flag(base + off[u]);
@@ -447,6 +451,27 @@ constexpr int kGatherU = 10;  // producer lines per warp per batch (16 warps x 1
 __device__ __forceinline__ void gather_y(const unsigned long long* src, const LayerDev& ly,
                                          float* dst, uint32_t seq, int* err) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (ly.R <= 32) {  // one 32-row segment per producer (every BASELINE config): cheap indices
+    const int R = ly.R, kmask = (1 << ly.ylog) - 1;
+    const bool kv = lane < R;
+    const int last = ly.fo - (ly.P - 1) * R;  // rows of the last producer
+    for (int pb = 0; pb < ly.P; pb += kWarps * kGatherU) {
+      int off[kGatherU];
+      unsigned long long v[kGatherU];
+#pragma unroll
+      for (int u = 0; u < kGatherU; u++) {
+        const int p = pb + warp + kWarps * u;
+        const bool ok = kv && p < ly.P && (p < ly.P - 1 || lane < last);
+        off[u] = ok ? (p << ly.ylog) + lane : -1;
+      }
+      poll_batch<kGatherU>(src, off, v, seq, err);
+#pragma unroll
+      for (int u = 0; u < kGatherU; u++)
+        if (off[u] >= 0) dst[(off[u] >> ly.ylog) * R + (off[u] & kmask)] =
+                             __uint_as_float((uint32_t)v[u]);
+    }
+    return;
+  }
   const int nseg = (ly.R + 31) >> 5, V = ly.P * nseg;
   for (int vb = 0; vb < V; vb += kWarps * kGatherU) {
     int off[kGatherU];
