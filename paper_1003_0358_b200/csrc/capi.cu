@@ -108,7 +108,7 @@ static int layout_smem(dmlp_net* net, unsigned mask, unsigned regmask = 0,
     d.delta_off[b] = take(maxr);
     d.dsc_off[b] = take(maxr);
   }
-  d.red_off = take(kWarps * 32);
+  d.red_off = take(2 * kWarps * 32);  // two: consecutive forward layers alternate
   d.pbuf_off = take(pb);
   d.out_off = take(4 * kMaxOut);
   LayerDev& lo = d.ly[L - 1];

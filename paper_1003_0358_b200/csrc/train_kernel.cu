@@ -178,22 +178,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         cp_async4(nx + i, X + (long long)img_nxt * ldx + i);
       cp_async_commit();
     }
+    PH(13);
 
     // ---------------- forward: hidden layers ----------------
     for (int l = 0; l < H; l++) {
       const LayerDev& ly = net.ly[l];
       const bool mine = c < ly.P;
-      if (l > 0) {  // gather y of layer l-1 (only row owners of l need it)
+      if (l > 0) {  // y of layer l-1: each thread polls the columns it consumes
         const LayerDev& lp = net.ly[l - 1];
         XB();
-        if (mine) gather_y(lp.yll + ((size_t)buf * lp.P << lp.ylog), lp, sm + ly.in_off, seq,
-                           net.err);
-        __syncthreads();
+        if (mine) {
+          const SrcSlots sl{lp.yll + ((size_t)buf * lp.P << lp.ylog), lp.R, lp.ylog, ly.fi};
+          if (ly.res == kResReg) gather_regcols<RC + RS>(sl, sm + ly.in_off, seq, net.err);
+          else gather_quads(sl, ly.pitch >> 2, ly.gs, sm + ly.in_off, seq, net.err);
+        }
         XE();
         PHL(4, l, 1);
         TRACE(2 + 2 * (l - 1));
       }
       if (mine) {
+        // consecutive layers alternate reduction buffers: no barrier is needed
+        // between this layer's writes and the previous layer's last reads
+        float* redl = red + (l & 1) * kWarps * 32;
         const float4* v4 = reinterpret_cast<const float4*>(l == 0 ? in0 : sm + ly.in_off);
         unsigned long long* ys =
             (l < H - 1) ? ly.yll + ((size_t)buf * ly.P << ly.ylog) + ((size_t)c << ly.ylog)
@@ -204,14 +210,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < NRL; i++)
             if (net.reg_layer[i] == l)
               reg_fwd<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.pitch, g_nr[l],
-                                  reinterpret_cast<const float*>(v4), red, sm + ly.t_off, yo,
+                                  reinterpret_cast<const float*>(v4), redl, sm + ly.t_off, yo,
                                   ys, seq);
         } else if (ly.res == kResSmem)
           fwd_dispatch<true>(reinterpret_cast<const float4*>(sm + ly.wsm_off), ly, g_nr[l], v4,
-                             red, sm + ly.t_off, yo, ys, seq, prof ? ph + 12 : nullptr);
+                             redl, sm + ly.t_off, yo, ys, seq, (prof && l == 0) ? ph + 14 : nullptr);
         else
           fwd_dispatch<false>(reinterpret_cast<const float4*>(ly.w + (size_t)g_r0[l] * ly.pitch),
-                              ly, g_nr[l], v4, red, sm + ly.t_off, yo, ys, seq);
+                              ly, g_nr[l], v4, redl, sm + ly.t_off, yo, ys, seq);
       }
       PHL(3, l, 0);
       if (l < H - 1) TRACE(1 + 2 * l);

@@ -177,16 +177,14 @@ __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, 
       const int k = gg + G * (j0 + jj);
       if (k < nr) {
         const float a = tree_sum<CH>(red + gg * WG * CH + jj, WG);
-        SUBP(1);
         float t;
         const float y = tanh_scaled_noinline(a, &t);
-        SUBP(2);
         tc[k] = t;
         if (yown) yown[k] = y;
         if (yslot) st_flag(yslot + k, y, seq);
       }
     }
-    SUBP(3);
+    SUBP(1);
     if (j0 + CH < njmax) __syncthreads();  // red is reused by the next chunk
   }
 #undef SUBP
@@ -491,6 +489,64 @@ __device__ __forceinline__ void gather_y(const unsigned long long* src, const La
       if (off[u] >= 0)
         dst[(off[u] >> ly.ylog) * ly.R + (off[u] & kmask)] = __uint_as_float((uint32_t)v[u]);
   }
+}
+
+// ---- own-column gather (forward) ---------------------------------------------
+// Every thread of a consuming CTA needs only the input columns of its own
+// quads (or register columns) -- the update of the same layer reads the same
+// columns from the same thread -- so it polls exactly those words from the
+// producers' slots and keeps them in its own smem positions.  No CTA barrier
+// separates the exchange from the dot: a thread starts as soon as its own
+// words have arrived, so the forward dot overlaps the tail of the exchange.
+struct SrcSlots {
+  const unsigned long long* src;  // this sample's [P][2^ylog] slots of the producing layer
+  int R, ylog, fi;                // producer rows, slot stride (log2 words), consumer fan-in
+};
+
+template <int U>
+__device__ __forceinline__ void gather_cols(const SrcSlots& sl, const int (&col)[U], float* v,
+                                            uint32_t seq, int* err) {
+  int off[U];
+#pragma unroll
+  for (int j = 0; j < U; j++) {
+    const int i = col[j];
+    if (i >= 0 && i < sl.fi) {
+      const int p = i / sl.R;
+      off[j] = (p << sl.ylog) + (i - p * sl.R);
+    } else {
+      off[j] = -1;
+    }
+  }
+  unsigned long long val[U];
+  poll_batch<U>(sl.src, off, val, seq, err);
+#pragma unroll
+  for (int j = 0; j < U; j++)
+    if (off[j] >= 0) v[col[j]] = __uint_as_float((uint32_t)val[j]);
+}
+
+// The float4 quads u, u+TG, ... of the RowMap thread, two per poll batch.
+__device__ __forceinline__ void gather_quads(const SrcSlots& sl, int nq, int gs, float* v,
+                                             uint32_t seq, int* err) {
+  const int TG = kThreads >> gs, u = threadIdx.x & (TG - 1);
+  for (int q = u; q < nq; q += 2 * TG) {
+    int col[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int qq = q + (j >> 2) * TG;
+      col[j] = qq < nq ? 4 * qq + (j & 3) : -1;
+    }
+    gather_cols<8>(sl, col, v, seq, err);
+  }
+}
+
+// The columns t + 512*m (m < NC) of a register row block.
+template <int NC>
+__device__ __forceinline__ void gather_regcols(const SrcSlots& sl, float* v, uint32_t seq,
+                                               int* err) {
+  int col[NC];
+#pragma unroll
+  for (int m = 0; m < NC; m++) col[m] = threadIdx.x + kThreads * m;
+  gather_cols<NC>(sl, col, v, seq, err);
 }
 
 // s_k = sum over producers c < P of src[c*stride + o + k], k < nr, in a
