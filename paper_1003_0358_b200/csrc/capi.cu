@@ -142,7 +142,9 @@ static void choose_mapping(LayerDev& ly) {
     // G > 1 stages G partial vectors in smem for the backward pass: only for
     // narrow layers, where the staging costs little shared memory
     if (G > 1 && G * ly.pitch > 2048) break;
-    const int cost = C * nj + (G > 1 ? 2 : 0) + 8 * ((nj + 15) / 16 - 1);
+    // G > 1 also costs a duplicated input gather and (backward) a staged
+    // combine of the partials: only worth it for a clear win
+    const int cost = C * nj + (G > 1 ? 4 : 0) + 8 * ((nj + 15) / 16 - 1);
     if (cost < best) {
       best = cost;
       ly.gs = gs;

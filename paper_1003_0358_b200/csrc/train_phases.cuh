@@ -397,17 +397,24 @@ template <int RR, int RC, int RS>
 __device__ __forceinline__ void reg_update(float (&w)[RR][RC], float* tail, int pitch, int nr,
                                            const float* __restrict__ v,
                                            const float* __restrict__ dsc) {
+  float sk[RR];  // eta*delta of the rows, read once (the tail stores may alias smem)
+#pragma unroll
+  for (int k = 0; k < RR; k++) sk[k] = k < nr ? dsc[k] : 0.0f;
+  float x[RC + RS];
 #pragma unroll
   for (int m = 0; m < RC + RS; m++) {
     const int c = threadIdx.x + kThreads * m;
-    const float x = c < pitch ? v[c] : 0.0f;
-#pragma unroll
-    for (int k = 0; k < RR; k++) {
-      const float sk = k < nr ? dsc[k] : 0.0f;
-      if (m < RC) w[k][m < RC ? m : 0] = upd(w[k][m < RC ? m : 0], sk, x);
-      else tail_at<RR, RS>(tail, m - RC, k) = upd(tail_at<RR, RS>(tail, m - RC, k), sk, x);
-    }
+    x[m] = c < pitch ? v[c] : 0.0f;
   }
+#pragma unroll
+  for (int k = 0; k < RR; k++)
+#pragma unroll
+    for (int m = 0; m < RC; m++) w[k][m] = upd(w[k][m], sk[k], x[m]);
+#pragma unroll
+  for (int m = RC; m < RC + RS; m++)
+#pragma unroll
+    for (int k = 0; k < RR; k++)
+      tail_at<RR, RS>(tail, m - RC, k) = upd(tail_at<RR, RS>(tail, m - RC, k), sk[k], x[m]);
 }
 
 // Poll a batch of U flag words per thread in rounds: every round re-issues
@@ -524,18 +531,51 @@ __device__ __forceinline__ void gather_cols(const SrcSlots& sl, const int (&col)
     if (off[j] >= 0) v[col[j]] = __uint_as_float((uint32_t)val[j]);
 }
 
-// The float4 quads u, u+TG, ... of the RowMap thread, two per poll batch.
+// The float4 quads u, u+TG, ... of the RowMap thread, one quad per poll
+// batch when the layer has one quad per thread, else two.  One division per
+// quad: its four columns are consecutive, so the producer index advances by
+// carry.
+__device__ __forceinline__ void quad_offsets(const SrcSlots& sl, int q, int (&off)[4]) {
+  const int i0 = 4 * q;
+  int p = i0 / sl.R, r = i0 - p * sl.R;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    off[j] = (i0 + j < sl.fi) ? (p << sl.ylog) + r : -1;
+    if (++r == sl.R) r = 0, p++;
+  }
+}
+
 __device__ __forceinline__ void gather_quads(const SrcSlots& sl, int nq, int gs, float* v,
                                              uint32_t seq, int* err) {
   const int TG = kThreads >> gs, u = threadIdx.x & (TG - 1);
-  for (int q = u; q < nq; q += 2 * TG) {
-    int col[8];
+  if (nq <= TG) {
+    if (u >= nq) return;
+    int off[4];
+    quad_offsets(sl, u, off);
+    unsigned long long val[4];
+    poll_batch<4>(sl.src, off, val, seq, err);
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const int qq = q + (j >> 2) * TG;
-      col[j] = qq < nq ? 4 * qq + (j & 3) : -1;
+    for (int j = 0; j < 4; j++)
+      if (off[j] >= 0) v[4 * u + j] = __uint_as_float((uint32_t)val[j]);
+    return;
+  }
+  for (int q = u; q < nq; q += 2 * TG) {
+    int off[8];
+    {
+      int o4[4];
+      quad_offsets(sl, q, o4);
+#pragma unroll
+      for (int j = 0; j < 4; j++) off[j] = o4[j];
+      if (q + TG < nq) quad_offsets(sl, q + TG, o4);
+      else o4[0] = o4[1] = o4[2] = o4[3] = -1;
+#pragma unroll
+      for (int j = 0; j < 4; j++) off[4 + j] = o4[j];
     }
-    gather_cols<8>(sl, col, v, seq, err);
+    unsigned long long val[8];
+    poll_batch<8>(sl.src, off, val, seq, err);
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      if (off[j] >= 0) v[4 * (q + (j >> 2) * TG) + (j & 3)] = __uint_as_float((uint32_t)val[j]);
   }
 }
 
