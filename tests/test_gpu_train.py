@@ -205,3 +205,33 @@ def test_train_epoch_headline_configs(golden, cfg):
     torch.cuda.synchronize()
     assert int(wrong.item()) == wrong_ref
     _assert_weights_close(dn.get_layers(), ref)
+
+
+@pytest.mark.parametrize("sizes,n_ctas", [
+    ((841, 10), 0),                      # no hidden layer: one CTA, output tile = all inputs
+    ((841, 5000, 10), 0),                # 34 rows per CTA: two reduction chunks, > 32-row gathers
+    ((841, 3000, 700, 10), 32),          # 94 / 22 rows per CTA on 32 CTAs
+    ((841, 37, 5, 9, 10), 0),            # layers narrower than the grid (P < 148), odd widths
+])
+def test_train_epoch_edge_shapes(golden, sizes, n_ctas):
+    import torch
+
+    g = golden("train")
+    x, lab = _inputs(golden)
+    # scale the uniform(+-0.05) init by fan-in so no output saturates: with
+    # saturated outputs argmax ties hinge on single ulps
+    ref = [(w * min(1.0, 841.0 / (w.shape[1] - 1)) ** 0.5).astype(np.float32)
+           for w in O.init_layers(4, sizes)]
+    dn = _net(sizes, [w.copy() for w in ref], n_ctas=n_ctas)
+    # 16 samples: functional coverage of the edge paths.  (Very wide single
+    # hidden layers are chaotic at eta = 1e-3: ulp-level differences in the
+    # 5000-term output sums grow ~10x every 6 steps -- scripts/diag_drift.py.)
+    order = np.arange(16) % 64
+    O.set_threads(8)
+    wrong_ref = O.train_epoch(ref, g["deformed"], lab, 1e-3, order=order)
+    wrong = torch.zeros((), dtype=torch.int64, device="cuda")
+    dn.train_epoch(torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda(),
+                   torch.from_numpy(order.astype(np.int32)).cuda(), 1e-3, wrong)
+    torch.cuda.synchronize()
+    assert int(wrong.item()) == wrong_ref
+    _assert_weights_close(dn.get_layers(), ref)
