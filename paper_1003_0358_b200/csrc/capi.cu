@@ -154,6 +154,101 @@ static void choose_mapping(LayerDev& ly) {
   ly.CH = nj <= 4 ? 4 : nj <= 8 ? 8 : 16;
 }
 
+// Row blocks, thread mappings and exchange-buffer offsets for nct CTAs.
+static void set_geometry(dmlp_net* net, int nct, size_t* yoff, size_t* poff) {
+  NetDev& d = net->dev;
+  const int H = d.L - 1;
+  d.nct = nct;
+  // exchange buffers (line-aligned per producer): y words [2][P][1<<ylog] for
+  // hidden layers but the last, output partials [2][P][1<<ylog], column
+  // partial words [2][P][pstride] for hidden layers l >= 1
+  size_t ll = 0;
+  for (int l = 0; l < H; l++) {
+    LayerDev& ly = d.ly[l];
+    ly.R = own_max_rows(ly.fo, nct);
+    ly.P = (ly.fo + ly.R - 1) / ly.R;
+    ly.ylog = ceil_log2(ly.R < 16 ? 16 : ly.R);
+    ly.pstride = round_up(ly.fi, 16);
+    choose_mapping(ly);
+    yoff[l] = ll;
+    if (l < H - 1) ll += 2 * (size_t)ly.P << ly.ylog;
+    if (l >= 1) {
+      poff[l] = ll;
+      ll += 2 * (size_t)ly.P * ly.pstride;
+    }
+  }
+  {
+    LayerDev& lo = d.ly[d.L - 1];
+    lo.R = H > 0 ? d.ly[H - 1].R : lo.fi;  // owned input columns per CTA
+    lo.P = H > 0 ? d.ly[H - 1].P : 1;
+    lo.ylog = ceil_log2(lo.fo < 16 ? 16 : lo.fo);
+    lo.gs = 0;
+    lo.CH = 1;
+    lo.pstride = 0;
+    yoff[d.L - 1] = ll;
+    ll += 2 * (size_t)lo.P << lo.ylog;
+  }
+  net->ll_words = ll;
+
+}
+
+// DMLP_RES_AUTO: keep the most weight bytes on chip.  For every compiled
+// register plan, put its row blocks on the largest layers that fit them, then
+// pick the best shared-memory subset of the rest; ties go to the simpler
+// plan.  Sets the plan on net; returns 2 if every hidden layer is on chip,
+// 1 if some is, 0 if none.
+static int auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
+  NetDev& d = net->dev;
+  const int H = d.L - 1;
+  unsigned mask = 0;
+  net->train_fn = nullptr;
+  net->reg_mask = 0;
+  net->reg_tail = 0;
+  long long best = -1;
+  const TrainVariant* vars = nullptr;
+  const int nv = train_variants(&vars);
+  for (int vi = 0; vi < nv; vi++) {
+    const TrainVariant& tv = vars[vi];
+    if (noreg && tv.n_reg > 0) continue;
+    unsigned regmask = 0;
+    long long regf = 0;
+    for (int i = 0; i < tv.n_reg; i++) {  // greedy: largest fitting layer not yet taken
+      int pick = -1;
+      long long pf = 0;
+      for (int l = 0; l < H; l++) {
+        const LayerDev& ly = d.ly[l];
+        if (((regmask >> l) & 1u) || ly.R > tv.rr || ly.pitch > kThreads * (tv.rc + tv.rs))
+          continue;
+        const long long f = (long long)ly.R * ly.pitch;
+        if (f > pf) { pf = f; pick = l; }
+      }
+      if (pick < 0) break;
+      regmask |= 1u << pick;
+      regf += pf;
+    }
+    if (tv.n_reg > 0 && regmask == 0) continue;
+    for (unsigned m = 0; m <= all; m++) {
+      if (m & regmask) continue;
+      if (layout_smem(net, m, regmask, tv.rr * tv.rs * kThreads) > smem_cap) continue;
+      const long long f = resident_floats(d, m) + regf;
+      if (f > best) {
+        best = f;
+        mask = m;
+        net->reg_mask = regmask;
+        net->train_fn = tv.fn;
+        net->reg_tail = tv.rr * tv.rs * kThreads;
+        for (int k = 0; k < kMaxRegLayers; k++) d.reg_layer[k] = -1;
+        int k = 0;
+        for (int l = 0; l < H; l++)
+          if ((regmask >> l) & 1u) d.reg_layer[k++] = l;
+      }
+    }
+  }
+  net->resident_mask = mask;
+  const unsigned onchip = mask | net->reg_mask;
+  return onchip == all ? 2 : onchip ? 1 : 0;
+}
+
 }  // namespace dmlp
 
 using namespace dmlp;
@@ -222,37 +317,8 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
   }
   net->w_floats = woff;
 
-  // exchange buffers (line-aligned per producer): y words [2][P][1<<ylog] for
-  // hidden layers but the last, output partials [2][P][1<<ylog], column
-  // partial words [2][P][pstride] for hidden layers l >= 1
-  size_t ll = 0;
   size_t yoff[kMaxLayers], poff[kMaxLayers];
-  for (int l = 0; l < H; l++) {
-    LayerDev& ly = d.ly[l];
-    ly.R = own_max_rows(ly.fo, nct);
-    ly.P = (ly.fo + ly.R - 1) / ly.R;
-    ly.ylog = ceil_log2(ly.R < 16 ? 16 : ly.R);
-    ly.pstride = round_up(ly.fi, 16);
-    choose_mapping(ly);
-    yoff[l] = ll;
-    if (l < H - 1) ll += 2 * (size_t)ly.P << ly.ylog;
-    if (l >= 1) {
-      poff[l] = ll;
-      ll += 2 * (size_t)ly.P * ly.pstride;
-    }
-  }
-  {
-    LayerDev& lo = d.ly[d.L - 1];
-    lo.R = H > 0 ? d.ly[H - 1].R : lo.fi;  // owned input columns per CTA
-    lo.P = H > 0 ? d.ly[H - 1].P : 1;
-    lo.ylog = ceil_log2(lo.fo < 16 ? 16 : lo.fo);
-    lo.gs = 0;
-    lo.CH = 1;
-    lo.pstride = 0;
-    yoff[d.L - 1] = ll;
-    ll += 2 * (size_t)lo.P << lo.ylog;
-  }
-  net->ll_words = ll;
+  set_geometry(net, nct, yoff, poff);
 
   // residency: choose which layers keep their rows in shared memory
   const int smem_cap = (int)prop.sharedMemPerBlockOptin - 1024;  // keep room for static smem
@@ -276,49 +342,19 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
                        need, smem_cap);
     }
   } else if (residency == DMLP_RES_AUTO) {
-    // Keep the most weight bytes on chip: for every compiled register plan,
-    // put its row blocks on the largest layers that fit them, then pick the
-    // best shared-memory subset of the rest.  Ties go to the simpler plan.
-    long long best = -1;
-    const TrainVariant* vars = nullptr;
-    const int nv = train_variants(&vars);
-    for (int vi = 0; vi < nv; vi++) {
-      const TrainVariant& tv = vars[vi];
-      if (noreg && tv.n_reg > 0) continue;
-      unsigned regmask = 0;
-      long long regf = 0;
-      for (int i = 0; i < tv.n_reg; i++) {  // greedy: largest fitting layer not yet taken
-        int pick = -1;
-        long long pf = 0;
-        for (int l = 0; l < H; l++) {
-          const LayerDev& ly = d.ly[l];
-          if (((regmask >> l) & 1u) || ly.R > tv.rr || ly.pitch > kThreads * (tv.rc + tv.rs))
-            continue;
-          const long long f = (long long)ly.R * ly.pitch;
-          if (f > pf) { pf = f; pick = l; }
-        }
-        if (pick < 0) break;
-        regmask |= 1u << pick;
-        regf += pf;
-      }
-      if (tv.n_reg > 0 && regmask == 0) continue;
-      for (unsigned m = 0; m <= all; m++) {
-        if (m & regmask) continue;
-        if (layout_smem(net, m, regmask, tv.rr * tv.rs * kThreads) > smem_cap) continue;
-        const long long f = resident_floats(d, m) + regf;
-        if (f > best) {
-          best = f;
-          mask = m;
-          net->reg_mask = regmask;
-          net->train_fn = tv.fn;
-          net->reg_tail = tv.rr * tv.rs * kThreads;
-          for (int k = 0; k < kMaxRegLayers; k++) d.reg_layer[k] = -1;
-          int k = 0;
-          for (int l = 0; l < H; l++)
-            if ((regmask >> l) & 1u) d.reg_layer[k++] = l;
-        }
+    // CTA count: with every weight on chip, 128-136 CTAs beat 148 (fewer
+    // producers per exchange, rows per CTA rounded to 8: profiles/r1 sweep);
+    // otherwise all SMs, for capacity.
+    if (n_ctas <= 0 && H > 0) {
+      for (int cand : {128, 136}) {
+        if (cand > prop.multiProcessorCount) continue;
+        set_geometry(net, cand, yoff, poff);
+        if (auto_plan(net, noreg, smem_cap, all) == 2) break;  // fully on chip
+        set_geometry(net, nct, yoff, poff);
       }
     }
+    auto_plan(net, noreg, smem_cap, all);
+    mask = net->resident_mask;
   }
   if (!net->train_fn) {
     const TrainVariant* vars = nullptr;
@@ -357,7 +393,7 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     return fail(rc);
   if ((rc = cuda_check(cudaMemset(net->d_w, 0, net->w_floats * sizeof(float)), "memset")))
     return fail(rc);
-  if (ll) {
+  if (const size_t ll = net->ll_words) {
     if ((rc = cuda_check(cudaMalloc(&net->d_ll, ll * 8), "cudaMalloc exchange"))) return fail(rc);
     if ((rc = cuda_check(cudaMemset(net->d_ll, 0, ll * 8), "memset"))) return fail(rc);
   }

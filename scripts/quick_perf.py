@@ -18,7 +18,7 @@ for name in names:
     rng = substream(0, 1)
     layers = [rng.uniform(-0.05, 0.05, size=(o, i + 1)).astype(np.float32) for i, o in zip(sizes[:-1], sizes[1:])]
     try:
-        dn = DeviceNet(sizes, residency=res)
+        dn = DeviceNet(sizes, residency=res, n_ctas=int(__import__("os").environ.get("NCT", "0")))
     except Exception as e:
         print(name, "create failed", e); continue
     dn.set_layers(layers)
