@@ -331,12 +331,7 @@ def run_gpu(args) -> dict | None:
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} {'-'.join(map(str, sizes))} on-line BP "
-                               f"(bs=1), {n} deformed synthetic digits per step",
-                   "weights": W, "samples_per_step": n,
-                   "parallelism": "replicas only" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (n*841*4 B per step); weights are "
-                         "deliberately kept in smem/L2"},
+        "config": bench_config(args, world),
         "e2e": {k: (round(v, 1) if isinstance(v, float) else v) for k, v in e2e.items()},
         "gpu_launches": args.steps,
         "roofline": roofline,
@@ -353,6 +348,18 @@ def run_gpu(args) -> dict | None:
     if world > 1:
         dist.destroy_process_group()
     return line
+
+
+def bench_config(args, world: int) -> dict:
+    """The workload description shared by both arms (same metric, same config)."""
+    sizes = CONFIGS[args.config]
+    n = args.samples
+    return {"workload": f"{args.config} {'-'.join(map(str, sizes))} on-line BP (bs=1), "
+                        f"{n} deformed synthetic digits per step",
+            "weights": count_weights(sizes), "samples_per_step": n,
+            "parallelism": "replicas only" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (n*841*4 B per step); weights are deliberately "
+                  "kept on chip (smem / registers) or in L2"}
 
 
 def l2_peak() -> float | None:
@@ -400,8 +407,7 @@ def run_reference(args) -> dict | None:
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * per, 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} {'-'.join(map(str, sizes))} on-line BP (bs=1)",
-                   "weights": W},
+        "config": bench_config(args, world),
         "cpu_baseline": cpu,
         "e2e": {"value": round(v, 3), "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
