@@ -122,3 +122,28 @@ def test_distributed_helpers_single_rank():
     counts = eval_counts_sharded(dn, full, lab).cpu().numpy()
     w, conf, sec, _ = O.eval_counts(O.forward_batch(layers, ref), labs)
     assert counts[0] == w and counts[101] == sec
+
+
+def test_train_resume_replays_the_uninterrupted_run(tmp_path):
+    """SPEC.md:517 resume path: 1 epoch + checkpoint + resume for epoch 2 gives
+    the same weights and history as 2 uninterrupted epochs."""
+    from paper_1003_0358_b200.mnist_io import Dataset
+    from paper_1003_0358_b200.network import Architecture, save_checkpoint
+    from paper_1003_0358_b200.trainer import TrainConfig, train
+    from paper_1003_0358_b200.synthetic import make_digits
+
+    imgs, labs = make_digits(400, seed=5)
+    sizes = (841, 90, 40, 10)
+    ds = Dataset(imgs, labs, "train")
+    full = train(TrainConfig(arch=Architecture(sizes), max_epochs=2), ds)
+    first = train(TrainConfig(arch=Architecture(sizes), max_epochs=1), ds)
+    # the state after epoch 0 (the last, not necessarily the best, weights)
+    ck = save_checkpoint(first.best_mlp if first.best_epoch == 0 else None, 0,
+                         first.history[0].val_error)
+    rest = train(TrainConfig(arch=Architecture(sizes), max_epochs=2), ds, resume=ck)
+    assert [h.epoch for h in rest.history] == [1]
+    assert rest.history[0].train_error == full.history[1].train_error
+    assert rest.history[0].val_error == full.history[1].val_error
+    if full.best_epoch == 1 and rest.best_epoch == 1:
+        for a, b in zip(full.best_mlp.layers, rest.best_mlp.layers):
+            assert np.array_equal(a, b)
