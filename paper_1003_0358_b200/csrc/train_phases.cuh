@@ -448,56 +448,6 @@ __device__ __forceinline__ void poll_batch(const unsigned long long* base, const
 
 constexpr int kGatherU = 10;  // producer lines per warp per batch (16 warps x 10 >= 148)
 
-// Gather y of hidden layer `ly` into dst (protocol E).  Producer p's rows sit
-// in its own line-aligned slot; each warp instruction reads one producer's
-// slot (lane = row within the block, 32-row segments when R > 32) and every
-// thread keeps all of its loads in flight, re-polling only the words whose
-// flag is not yet this sample's.
-__device__ __forceinline__ void gather_y(const unsigned long long* src, const LayerDev& ly,
-                                         float* dst, uint32_t seq, int* err) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (ly.R <= 32) {  // one 32-row segment per producer (every BASELINE config): cheap indices
-    const int R = ly.R, kmask = (1 << ly.ylog) - 1;
-    const bool kv = lane < R;
-    const int last = ly.fo - (ly.P - 1) * R;  // rows of the last producer
-    for (int pb = 0; pb < ly.P; pb += kWarps * kGatherU) {
-      int off[kGatherU];
-      unsigned long long v[kGatherU];
-#pragma unroll
-      for (int u = 0; u < kGatherU; u++) {
-        const int p = pb + warp + kWarps * u;
-        const bool ok = kv && p < ly.P && (p < ly.P - 1 || lane < last);
-        off[u] = ok ? (p << ly.ylog) + lane : -1;
-      }
-      poll_batch<kGatherU>(src, off, v, seq, err);
-#pragma unroll
-      for (int u = 0; u < kGatherU; u++)
-        if (off[u] >= 0) dst[(off[u] >> ly.ylog) * R + (off[u] & kmask)] =
-                             __uint_as_float((uint32_t)v[u]);
-    }
-    return;
-  }
-  const int nseg = (ly.R + 31) >> 5, V = ly.P * nseg;
-  for (int vb = 0; vb < V; vb += kWarps * kGatherU) {
-    int off[kGatherU];
-    unsigned long long v[kGatherU];
-#pragma unroll
-    for (int u = 0; u < kGatherU; u++) {
-      const int vi = vb + warp + kWarps * u;
-      const int p = nseg == 1 ? vi : vi / nseg;
-      const int k = (vi - p * nseg) * 32 + lane;
-      const bool ok = vi < V && k < ly.R && p * ly.R + k < ly.fo;
-      off[u] = ok ? (p << ly.ylog) + k : -1;
-    }
-    poll_batch<kGatherU>(src, off, v, seq, err);
-    const int kmask = (1 << ly.ylog) - 1;
-#pragma unroll
-    for (int u = 0; u < kGatherU; u++)  // slot offset -> row: p * R + k
-      if (off[u] >= 0)
-        dst[(off[u] >> ly.ylog) * ly.R + (off[u] & kmask)] = __uint_as_float((uint32_t)v[u]);
-  }
-}
-
 // ---- own-column gather (forward) ---------------------------------------------
 // Every thread of a consuming CTA needs only the input columns of its own
 // quads (or register columns) -- the update of the same layer reads the same

@@ -5,7 +5,7 @@
 // kernel's compute+publish+gather sequence.  mode 0: compute + exchange,
 // mode 1: exchange only (publish zeros), mode 2: compute only.
 #include <cstdio>
-#include "train_phases.cuh"
+#include "mb_common.cuh"
 using namespace dmlp;
 
 __global__ void __launch_bounds__(512, 1) k_x(int R, int pitch, int NL, unsigned long long* buf,

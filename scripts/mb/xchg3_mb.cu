@@ -1,5 +1,5 @@
 #include <cstdio>
-#include "train_phases.cuh"
+#include "mb_common.cuh"
 using namespace dmlp;
 // V0: sync, publish, gather (static dst); V1: no pre-publish sync; V2: dynamic dst;
 // V3: publish by threads 0..R-1 then gather into dynamic smem, no pre-sync (xchg2 mode 1)

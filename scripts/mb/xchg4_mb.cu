@@ -1,7 +1,7 @@
 // Does the all-to-all exchange get cheaper with fewer (bigger) producers?
 // NP producer CTAs publish R words each (same total words), all 148 CTAs gather.
 #include <cstdio>
-#include "train_phases.cuh"
+#include "mb_common.cuh"
 using namespace dmlp;
 __global__ void __launch_bounds__(512, 1) k_x(LayerDev ly, unsigned long long* buf, int iters,
                                                long long* out, int* err) {

@@ -3,7 +3,7 @@
 // gathers every producer's words with the kernel's own gather_y (protocol E)
 // or a variant.  Reports cycles per iteration (slowest CTA).
 #include <cstdio>
-#include "train_phases.cuh"
+#include "mb_common.cuh"
 using namespace dmlp;
 
 __device__ __forceinline__ void spin(long long cyc) {
