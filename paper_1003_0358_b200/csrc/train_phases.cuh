@@ -500,6 +500,29 @@ __device__ __forceinline__ void gather_quads(const SrcSlots& sl, int nq, int gs,
   const int TG = kThreads >> gs, u = threadIdx.x & (TG - 1);
   if (nq <= TG) {
     if (u >= nq) return;
+    if ((sl.R & 3) == 0 && 4 * u + 4 <= sl.fi) {
+      // producer blocks of a multiple of 4 rows: the quad is 4 consecutive,
+      // 32-byte aligned words of one producer's slot -> two vector polls
+      const int p = 4 * u / sl.R;
+      const unsigned long long* a = sl.src + (p << sl.ylog) + (4 * u - p * sl.R);
+      unsigned long long w0, w1, w2, w3;
+      long long t0 = 0;
+      for (int round = 0;; round++) {
+        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                     : "=l"(w0), "=l"(w1) : "l"(a) : "memory");
+        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                     : "=l"(w2), "=l"(w3) : "l"(a + 2) : "memory");
+        if ((uint32_t)(w0 >> 32) == seq && (uint32_t)(w1 >> 32) == seq &&
+            (uint32_t)(w2 >> 32) == seq && (uint32_t)(w3 >> 32) == seq)
+          break;
+        if (round == 0) t0 = clock64();
+        else if (clock64() - t0 > kSpinTimeoutCycles) spin_fail(err);
+      }
+      reinterpret_cast<float4*>(v)[u] =
+          make_float4(__uint_as_float((uint32_t)w0), __uint_as_float((uint32_t)w1),
+                      __uint_as_float((uint32_t)w2), __uint_as_float((uint32_t)w3));
+      return;
+    }
     int off[4];
     quad_offsets(sl, u, off);
     unsigned long long val[4];
