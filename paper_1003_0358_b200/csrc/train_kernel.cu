@@ -422,6 +422,7 @@ static const TrainVariant kVariants[] = {
     {1, 14, 4, 1, (const void*)k_train<1, 14, 4, 1>},
     {2, 7, 2, 0, (const void*)k_train<2, 7, 2, 0>},
     {4, 7, 2, 0, (const void*)k_train<4, 7, 2, 0>},
+    {3, 8, 2, 0, (const void*)k_train<3, 8, 2, 0>},
 };
 
 int train_variants(const TrainVariant** out) {
