@@ -155,6 +155,18 @@ int dmlp_bench(int32_t kind, int64_t bytes, int32_t iters, int32_t n_ctas, doubl
  * reduction, [4] dependent L2 load, [5] dependent ld.relaxed.gpu, [6] smem load. */
 int dmlp_bench_prims(double *out);
 
+/* ---- fp64 gradient-check oracle (kernels.backprop_gradients / gradient_check,
+ * kernels.py:374-418), a debug aid for small nets (every layer <= 1024 units).
+ * sizes: layer sizes (input first); w_host: float64 weights of every layer in
+ * the reference layout (fo, fi+1), bias last, concatenated; x_host: float64
+ * input.  grad_bp / grad_fd (optional, host, one float64 per weight): the
+ * analytic gradient of E = 0.5*sum((y - t)^2) and the central finite
+ * difference with `step`; *worst = max |g_bp - g_fd| / max(|g_bp|, |g_fd|,
+ * 1e-8).  Synchronous. */
+int dmlp_gradient_check(const int32_t *sizes, int32_t n_sizes, const double *w_host,
+                        const double *x_host, int32_t digit, double step, double *grad_bp,
+                        double *grad_fd, double *worst);
+
 /* Device tanhf checks: the select-form kernel tanhf against its branchy
  * glibc restatement on all 2^32 inputs (NaN payloads aside), and evaluation
  * on given inputs (device pointers) for comparison with the host libm. */

@@ -28,6 +28,7 @@ UNITS = {
     "eval_kernel.cu": [],
     "deform_kernel.cu": ["-fmad=false"],
     "microbench.cu": [],
+    "gradcheck_kernel.cu": [],
 }
 
 

@@ -158,10 +158,26 @@ def gen_eval_and_known():
     )
 
 
+def gen_gradcheck():
+    """kernels.backprop_gradients / gradient_check on a tiny float64 net."""
+    arch = network.Architecture((24, 9, 7, 10))
+    mlp = network.init_mlp(rng.substream(9, rng.STREAM_INIT), arch).astype(np.float64)
+    mlp.layers = [w * 4.0 for w in mlp.layers]  # away from the linear regime
+    x = rng.substream(9, 4).uniform(-1.0, 1.0, size=24)
+    digit = 3
+    grads = kernels.backprop_gradients(mlp, x, digit)
+    worst = kernels.gradient_check(mlp, x, digit, step=1e-5)
+    np.savez_compressed(os.path.join(OUT, "gradcheck.npz"), sizes=np.array(arch.layer_sizes),
+                        weights=np.concatenate([w.ravel() for w in mlp.layers]), x=x,
+                        digit=np.int64(digit), grads=np.concatenate([g.ravel() for g in grads]),
+                        worst=np.float64(worst))
+
+
 if __name__ == "__main__":
     gen_rng()
     gen_deform()
     gen_train()
     gen_eval_and_known()
+    gen_gradcheck()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

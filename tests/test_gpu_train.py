@@ -235,3 +235,24 @@ def test_train_epoch_edge_shapes(golden, sizes, n_ctas):
     torch.cuda.synchronize()
     assert int(wrong.item()) == wrong_ref
     _assert_weights_close(dn.get_layers(), ref)
+
+
+def test_gradient_check_oracle_on_gpu(golden):
+    """kernels.backprop_gradients / gradient_check in float64 on the GPU vs the
+    reference's own values (tests/golden/gradcheck.npz, made by the reference)."""
+    from paper_1003_0358_b200 import kernels
+    from paper_1003_0358_b200.network import Architecture, Mlp
+
+    g = golden("gradcheck")
+    arch = Architecture(tuple(int(v) for v in g["sizes"]))
+    layers, pos = [], 0
+    for fo, fi1 in arch.layer_shapes():
+        layers.append(g["weights"][pos:pos + fo * fi1].reshape(fo, fi1).astype(np.float64))
+        pos += fo * fi1
+    mlp = Mlp(arch, layers)
+    grads = np.concatenate([a.ravel() for a in kernels.backprop_gradients(mlp, g["x"],
+                                                                         int(g["digit"]))])
+    np.testing.assert_allclose(grads, g["grads"], rtol=1e-11, atol=1e-14)
+    worst = kernels.gradient_check(mlp, g["x"], int(g["digit"]), step=1e-5)
+    ref = float(g["worst"])
+    assert worst < 1e-6 and ref / 10 <= worst <= ref * 10, (worst, ref)
