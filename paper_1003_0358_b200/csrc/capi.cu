@@ -595,6 +595,7 @@ static int run_epoch(dmlp_net* net, const float* x, long long ldx, const uint8_t
                      const int32_t* order, long long n, float eta, long long* wrong, float* y_last,
                      cudaStream_t st) {
   if (n <= 0) return DMLP_OK;
+  if (n > 0x7FFFFFFFLL) return set_error(DMLP_EINVAL, "at most 2^31-1 samples per launch");
   if (!(eta >= 0.0f)) return set_error(DMLP_EINVAL, "eta must be non-negative");
   if (ldx < net->sizes[0]) return set_error(DMLP_ESIZE, "row stride %lld < fan-in %d", ldx,
                                             net->sizes[0]);
