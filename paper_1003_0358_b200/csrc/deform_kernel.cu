@@ -178,7 +178,7 @@ __device__ void deform_from_draws(DefSmem& S, int ks, float* out) {
   }
 }
 
-__global__ void __launch_bounds__(kDefThreads)
+__global__ void __launch_bounds__(kDefThreads, 4)
     k_deform(const uint8_t* __restrict__ raw, const uint8_t* __restrict__ labels, long long first,
              long long n, unsigned long long seed, unsigned long long epoch, DefP P,
              float* __restrict__ out) {
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kDefThreads)
   }
 }
 
-__global__ void __launch_bounds__(kDefThreads)
+__global__ void __launch_bounds__(kDefThreads, 4)
     k_deform_injected(const uint8_t* __restrict__ raw, long long n, const double* __restrict__ ndx,
                       const double* __restrict__ ndy, const double* __restrict__ scal, int ks,
                       float* __restrict__ out) {
