@@ -60,7 +60,8 @@ def main():
         v = float(m[k]["value"].replace(",", ""))
         u = m[k]["unit"].lower()
         f = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "ms": 1e-3, "us": 1e-6,
-             "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "nsecond": 1e-9, "s": 1}.get(u, 1)
+             "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "nsecond": 1e-9, "s": 1,
+             "ghz": 1e9, "mhz": 1e6}.get(u, 1)
         return v * f / scale
 
     dram = (num("dram__bytes_read.sum", 1) or 0) + (num("dram__bytes_write.sum", 1) or 0)
@@ -73,6 +74,15 @@ def main():
            "stall_reason_share": stall, "metrics": m}
     if a.algo_bytes and t:
         out["achieved_GBs_under_ncu"] = a.algo_bytes * a.units / t / 1e9
+    if t:
+        # achieved shared-memory and L2 bandwidth of the launch (128 B per smem
+        # wavefront, 32 B per L2 sector) against the B200 peaks: smem 128 B/clk
+        # per SM (148 SMs at the measured clock), L2 from MEASURED r+w (K6)
+        clk = num("sm__cycles_elapsed.avg.per_second", 1) or 1.965e9
+        wav = num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1) or 0.0
+        out["smem_GBs"] = round(128 * wav / t / 1e9, 1)
+        out["smem_peak_GBs"] = round(148 * 128 * clk / 1e9, 1)
+        out["l2_GBs"] = round(32 * (num("lts__t_sectors.sum", 1) or 0) / t / 1e9, 1)
     with open(a.out, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "metrics"}))
