@@ -212,6 +212,8 @@ static double auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
   for (int vi = 0; vi < nv; vi++) {
     const TrainVariant& tv = vars[vi];
     if (noreg && tv.n_reg > 0) continue;
+    if (const char* fv = getenv("DMLP_FORCE_VARIANT"))  // experiments: only plan `fv`
+      if (atoi(fv) != vi) continue;
     unsigned regmask = 0;
     long long regf = 0;
     for (int i = 0; i < tv.n_reg; i++) {  // greedy: largest fitting layer not yet taken
@@ -233,7 +235,9 @@ static double auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
       if (m & regmask) continue;
       if (layout_smem(net, m, regmask, tv.rr * tv.rs * kThreads) > smem_cap) continue;
       const long long f = resident_floats(d, m) + regf;
-      if (f > best) {
+      // ties go to the simpler plan, except that a plan holding every hidden
+      // layer in registers beats shared memory (C1: +5%; CTA-count sweep)
+      if (f > best || (f == best && regmask == all && net->reg_mask != all)) {
         best = f;
         mask = m;
         net->reg_mask = regmask;
