@@ -182,14 +182,16 @@ def test_device_tanhf_matches_libm():
     assert same.all(), x[~same][:5]
 
 
-@pytest.mark.parametrize("cfg", ["C4", "C5"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
 def test_train_epoch_headline_configs(golden, cfg):
-    """The BASELINE configs with their auto residency (register row blocks,
-    shared memory and streamed layers): 160 on-line samples in one launch vs
-    the oracle's epoch on identical inputs."""
+    """The BASELINE configs with their auto plans (CTA count, register row
+    blocks, shared memory and streamed layers): 160 on-line samples in one
+    launch vs the oracle's epoch on identical inputs."""
     import torch
 
-    sizes = {"C4": (841, 2500, 2000, 1500, 1000, 500, 10),
+    sizes = {"C1": (841, 1000, 500, 10), "C2": (841, 1500, 1000, 500, 10),
+             "C3": (841, 2000, 1500, 1000, 500, 10),
+             "C4": (841, 2500, 2000, 1500, 1000, 500, 10),
              "C5": (841,) + (1000,) * 9 + (10,)}[cfg]
     g = golden("train")
     x, lab = _inputs(golden)
