@@ -85,8 +85,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
   for (int i = 0; i < NRL; i++) {  // register-resident row blocks
     const int l = net.reg_layer[i];
-    const LayerDev& ly = net.ly[l < 0 ? 0 : l];
-    const int r0 = min(c * ly.R, ly.fo), nr = l < 0 ? 0 : min(ly.R, ly.fo - r0);
+    if (l < 0) {  // slot unused by this net's plan
+#pragma unroll
+      for (int k = 0; k < RR; k++)
+#pragma unroll
+        for (int m = 0; m < RC; m++) wr[i][k][m] = 0.0f;
+      continue;
+    }
+    const LayerDev& ly = net.ly[l];
+    const int r0 = min(c * ly.R, ly.fo), nr = min(ly.R, ly.fo - r0);
     reg_load<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.w + (size_t)r0 * ly.pitch, ly.pitch, nr);
   }
   for (int l = 0; l < H; l++) {  // smem-resident hidden layers: load the rows once
