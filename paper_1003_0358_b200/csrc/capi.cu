@@ -351,12 +351,13 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
                        need, smem_cap);
     }
   } else if (residency == DMLP_RES_AUTO) {
-    // CTA count: with every weight on chip, 128-136 CTAs beat 148 (fewer
-    // producers per exchange, rows per CTA rounded to 8: profiles/r1 sweep);
-    // otherwise all SMs, for capacity.
-    // Rows per CTA rounded up to a multiple of 4 (producer blocks polled as
-    // 16-byte vectors, fewer producers) pay when >= 90% of the weights stay
-    // on chip (C5: +4.4%), not when the extra rows push layers to L2 (C4).
+    // Grid and row blocks (CTA-count and rounding sweeps):
+    //  1. 128 (then 136) CTAs when every weight fits on chip with that many:
+    //     fewer producers per exchange (C1-C3: 6-10% faster than 148);
+    //  2. else all SMs with rows per CTA rounded up to a multiple of 4
+    //     (producer blocks polled as 16-byte vectors, fewer producers) when
+    //     >= 90% of the weights stay on chip (C5: +4.4%);
+    //  3. else all SMs, rows per CTA = ceil(fo / SMs), for capacity (C4).
     bool chosen = false;
     if (n_ctas <= 0 && H > 0) {
       for (int cand : {128, 136}) {
