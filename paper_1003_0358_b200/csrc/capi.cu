@@ -204,6 +204,7 @@ static double auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
   const int H = d.L - 1;
   unsigned mask = 0;
   net->train_fn = nullptr;
+  net->train_fn_prof = nullptr;
   net->reg_mask = 0;
   net->reg_tail = 0;
   long long best = -1;
@@ -242,6 +243,7 @@ static double auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
         mask = m;
         net->reg_mask = regmask;
         net->train_fn = tv.fn;
+        net->train_fn_prof = tv.fn_prof;
         net->reg_tail = tv.rr * tv.rs * kThreads;
         for (int k = 0; k < kMaxRegLayers; k++) d.reg_layer[k] = -1;
         int k = 0;
@@ -381,6 +383,7 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     const TrainVariant* vars = nullptr;
     train_variants(&vars);
     net->train_fn = vars[0].fn;
+    net->train_fn_prof = vars[0].fn_prof;
     for (int k = 0; k < kMaxRegLayers; k++) d.reg_layer[k] = -1;
   }
   if (layout_smem(net, 0) > smem_cap) {
@@ -401,6 +404,8 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     return code;
   };
   if ((rc = cuda_check(set_train_attributes(net->train_fn, net->smem_bytes),
+                       "cudaFuncSetAttribute")) ||
+      (rc = cuda_check(set_train_attributes(net->train_fn_prof, net->smem_bytes),
                        "cudaFuncSetAttribute")))
     return fail(rc);
   int bps = 0;

@@ -89,7 +89,8 @@ struct dmlp_net {
   unsigned resident_mask = 0;
   unsigned reg_mask = 0;
   int reg_tail = 0;  // floats of shared-memory tail per register row block
-  const void* train_fn = nullptr;  // selected TrainVariant
+  const void* train_fn = nullptr;       // selected TrainVariant
+  const void* train_fn_prof = nullptr;  // its profiling instance
   uint32_t seq = 1;  // next sample sequence number (flag value)
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;  // recorded after every operation on the net, whatever the stream
@@ -115,7 +116,8 @@ cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
 // slots per thread in shared memory.
 struct TrainVariant {
   int n_reg, rr, rc, rs;  // rs: column slots of each block kept in a shared-memory tail
-  const void* fn;
+  const void* fn;         // the kernel without the profile / trace hooks
+  const void* fn_prof;    // with them (launched while profiling or tracing)
 };
 int train_variants(const TrainVariant** out);
 cudaError_t set_train_attributes(const void* fn, int smem_bytes);

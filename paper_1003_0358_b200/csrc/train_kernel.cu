@@ -41,7 +41,10 @@
 namespace dmlp {
 
 constexpr int kProfSlots = kProfWords;
-template <int NRL, int RR, int RC, int RS>
+// PROF: the in-kernel phase profile and the one-sample timeline are compiled
+// in (selected only while profiling or tracing is enabled: the hooks cost
+// 1.5-7.5% even when switched off at run time).
+template <int NRL, int RR, int RC, int RS, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_train(const NetDev net, const float* __restrict__ X, long long ldx,
             const uint8_t* __restrict__ labels, const int32_t* __restrict__ order,
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool counter = (c == 0 && tid == kThreads - 1);
   // optional in-kernel profile (thread 0 of every CTA): per-phase cycles.
   // slot 0 loop total, 1 exchange waits; 2.. per phase (device.py names them).
-  const bool prof = net.prof != nullptr && tid == 0;
+  const bool prof = PROF && net.prof != nullptr && tid == 0;
   __shared__ long long ph[kProfSlots];  // per-phase cycles (thread 0 only)
   for (int i = tid; i < kProfSlots; i += kThreads) ph[i] = 0;
   // thread 0's clocks live in smem: no registers held across the loop
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // gather done (forward y exchanges e = 0..L-3, output partials e = L-2,
   // backward e = L-1..2L-4); 63 sample end.
 #define TRACE(mark)                                                          \
-  if (net.trace != nullptr && s == net.trace_sample) {                      \
+  if (PROF && net.trace != nullptr && s == net.trace_sample) {              \
     __syncthreads();                                                          \
     if (tid == 0) {                                                           \
       unsigned long long _g;                                                  \
@@ -424,13 +427,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // slots + 1 shared-memory slot (the 2000x2501 hidden layer of C4: 14 rows x
 // 2504 columns per CTA); and up to four 7-row x 2-column blocks (1000-wide
 // layers: C5).
+#define DMLP_VARIANT(n, rr, rc, rs)                                            \
+  {n, rr, rc, rs, (const void*)k_train<n, rr, rc, rs, false>,                  \
+   (const void*)k_train<n, rr, rc, rs, true>}
 static const TrainVariant kVariants[] = {
-    {0, 1, 1, 0, (const void*)k_train<0, 1, 1, 0>},
-    {1, 14, 4, 1, (const void*)k_train<1, 14, 4, 1>},
-    {2, 7, 2, 0, (const void*)k_train<2, 7, 2, 0>},
-    {4, 7, 2, 0, (const void*)k_train<4, 7, 2, 0>},
-    {3, 8, 2, 0, (const void*)k_train<3, 8, 2, 0>},
+    DMLP_VARIANT(0, 1, 1, 0), DMLP_VARIANT(1, 14, 4, 1), DMLP_VARIANT(2, 7, 2, 0),
+    DMLP_VARIANT(4, 7, 2, 0), DMLP_VARIANT(3, 8, 2, 0),
 };
+#undef DMLP_VARIANT
 
 int train_variants(const TrainVariant** out) {
   *out = kVariants;
@@ -451,7 +455,8 @@ cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
   NetDev nd = net->dev;
   unsigned long long* w = reinterpret_cast<unsigned long long*>(wrong);
   void* args[] = {&nd, &x, &ldx, &labels, &order, &n, &eta, &seq0, &w, &y_last};
-  return cudaLaunchCooperativeKernel(net->train_fn, dim3(nd.nct), dim3(kThreads), args,
+  const void* fn = (nd.prof || nd.trace) ? net->train_fn_prof : net->train_fn;
+  return cudaLaunchCooperativeKernel(fn, dim3(nd.nct), dim3(kThreads), args,
                                      (size_t)net->smem_bytes, st);
 }
 
