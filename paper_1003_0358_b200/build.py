@@ -11,6 +11,7 @@ reference's rounding must be reproduced.
 
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -24,7 +25,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 UNITS = {
     "capi.cu": [],
-    "train_kernel.cu": [],
+    "train_inst_f0.cu": [],
+    "train_inst_f1.cu": [],
+    "train_inst_f3.cu": [],
+    "train_glue.cu": [],
     "eval_kernel.cu": [],
     "deform_kernel.cu": ["-fmad=false"],
     "microbench.cu": [],
@@ -43,19 +47,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "dmlp.h"))
-    objs = []
+    objs, jobs = [], []
     for unit, flags in UNITS.items():
         src = os.path.join(CSRC, unit)
         obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            cmd = [NVCC, *ARCH, *COMMON, *flags, "-Xptxas", "-v" if verbose else "-O3",
-                   "-c", src, "-o", obj]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                raise RuntimeError(f"nvcc failed for {unit}:\n{r.stdout}\n{r.stderr}")
+            jobs.append((unit, [NVCC, *ARCH, *COMMON, *flags, "-Xptxas",
+                                "-v" if verbose else "-O3", "-c", src, "-o", obj]))
+
+    def compile_unit(job):
+        unit, cmd = job
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {unit}:\n{r.stdout}\n{r.stderr}")
+        return r.stderr
+
+    # the training-kernel instances dominate the build: compile the units in parallel
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+        for err in ex.map(compile_unit, jobs):
             if verbose:
-                sys.stderr.write(r.stderr)
+                sys.stderr.write(err)
     if force or _stale(OUT, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)

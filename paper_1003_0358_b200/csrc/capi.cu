@@ -204,7 +204,6 @@ static double auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
   const int H = d.L - 1;
   unsigned mask = 0;
   net->train_fn = nullptr;
-  net->train_fn_prof = nullptr;
   net->reg_mask = 0;
   net->reg_tail = 0;
   long long best = -1;
@@ -242,8 +241,8 @@ static double auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
         best = f;
         mask = m;
         net->reg_mask = regmask;
-        net->train_fn = tv.fn;
-        net->train_fn_prof = tv.fn_prof;
+        net->variant = vi;
+        net->train_fn = tv.fn[3];
         net->reg_tail = tv.rr * tv.rs * kThreads;
         for (int k = 0; k < kMaxRegLayers; k++) d.reg_layer[k] = -1;
         int k = 0;
@@ -382,8 +381,8 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
   if (!net->train_fn) {
     const TrainVariant* vars = nullptr;
     train_variants(&vars);
-    net->train_fn = vars[0].fn;
-    net->train_fn_prof = vars[0].fn_prof;
+    net->variant = 0;
+    net->train_fn = vars[0].fn[3];
     for (int k = 0; k < kMaxRegLayers; k++) d.reg_layer[k] = -1;
   }
   if (layout_smem(net, 0) > smem_cap) {
@@ -397,6 +396,16 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
       onchip == all ? DMLP_RES_SMEM : (onchip == 0 ? DMLP_RES_L2 : DMLP_RES_HYBRID);
   net->smem_bytes = layout_smem(net, mask, net->reg_mask, net->reg_tail);
   net->resident_mask = mask;
+  {  // the instance compiled with just the residency paths this plan uses
+    const TrainVariant* vars = nullptr;
+    train_variants(&vars);
+    int feat = 0;
+    for (int l = 0; l < H; l++)
+      feat |= d.ly[l].res == kResSmem ? kFeatSmem : d.ly[l].res == kResL2 ? kFeatL2 : 0;
+    if (const char* f = getenv("DMLP_FEAT")) feat |= atoi(f);  // debugging aid: more paths
+    net->train_fn = train_instance(vars[net->variant], feat);
+    net->train_fn_prof = vars[net->variant].fn_prof;
+  }
 
   int rc = DMLP_OK;
   auto fail = [&](int code) {

@@ -89,7 +89,8 @@ struct dmlp_net {
   unsigned resident_mask = 0;
   unsigned reg_mask = 0;
   int reg_tail = 0;  // floats of shared-memory tail per register row block
-  const void* train_fn = nullptr;       // selected TrainVariant
+  int variant = 0;                      // selected TrainVariant
+  const void* train_fn = nullptr;       // its instance for the net's feature set
   const void* train_fn_prof = nullptr;  // its profiling instance
   uint32_t seq = 1;  // next sample sequence number (flag value)
   cudaStream_t stream = nullptr;
@@ -114,12 +115,15 @@ cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
 // Compiled instantiations of the training kernel: n_reg register row blocks
 // of at most rr rows x rc columns per thread (0 = none), plus rs column
 // slots per thread in shared memory.
+enum { kFeatSmem = 1, kFeatL2 = 2 };  // residency paths compiled into an instance
 struct TrainVariant {
   int n_reg, rr, rc, rs;  // rs: column slots of each block kept in a shared-memory tail
-  const void* fn;         // the kernel without the profile / trace hooks
-  const void* fn_prof;    // with them (launched while profiling or tracing)
+  const void* fn[4];      // by feature set (kFeatSmem | kFeatL2), no profile hooks; may be null
+  const void* fn_prof;    // every feature plus the profile / trace hooks
 };
 int train_variants(const TrainVariant** out);
+// The instance of plan tv compiled with the fewest features covering `feat`.
+const void* train_instance(const TrainVariant& tv, int feat);
 cudaError_t set_train_attributes(const void* fn, int smem_bytes);
 cudaError_t train_occupancy(const void* fn, int smem_bytes, int* blocks_per_sm);
 }  // namespace dmlp

@@ -1,4 +1,7 @@
-// train_kernel.cu -- persistent on-line back-propagation kernel (sm_100a).
+// train_kernel.cuh -- persistent on-line back-propagation kernel (sm_100a).
+//
+// The kernel template; train_inst_f*.cu instantiate it (one translation unit
+// per feature set, compiled in parallel) and train_glue.cu launches it.
 //
 // Replaces trainer.train_epoch's per-sample Python loop (trainer.py:104-123)
 // and kernels.train_step (kernels.py:329-361): ONE launch trains a whole
@@ -32,6 +35,7 @@
 //    words start on their own 128-byte line (one writer per polled line),
 //    buffers alternate by sample parity, and every consumer keeps all its
 //    polls in flight (protocol E, profiles/r1_microbench.json).
+#pragma once
 #include <cuda_runtime.h>
 
 #include "dmlp_internal.h"
@@ -41,10 +45,14 @@
 namespace dmlp {
 
 constexpr int kProfSlots = kProfWords;
+// FEAT: which residency paths are compiled in (kFeatSmem: shared-memory
+// hidden layers, kFeatL2: L2-streamed ones; register row blocks always):
+// code a net never runs still costs registers and instruction fetch in the
+// hot loop (C1, registers only: +8.8% without the smem/L2 paths).
 // PROF: the in-kernel phase profile and the one-sample timeline are compiled
 // in (selected only while profiling or tracing is enabled: the hooks cost
 // 1.5-7.5% even when switched off at run time).
-template <int NRL, int RR, int RC, int RS, bool PROF>
+template <int NRL, int RR, int RC, int RS, int FEAT, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_train(const NetDev net, const float* __restrict__ X, long long ldx,
             const uint8_t* __restrict__ labels, const int32_t* __restrict__ order,
@@ -52,6 +60,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float* y_last) {
   extern __shared__ __align__(16) float sm[];
   __shared__ int g_r0[kMaxLayers], g_nr[kMaxLayers];
+  __shared__ int g_rb[kMaxLayers];  // forward reduction buffer offset per layer
   const int c = blockIdx.x, tid = threadIdx.x;
   const int L = net.L, H = L - 1;  // H hidden layers
   float* red = sm + net.red_off;
@@ -67,6 +76,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r0 = min(c * ly.R, ly.fo);
     g_r0[tid] = r0;
     g_nr[tid] = min(ly.R, ly.fo - r0);
+    int nown = 0;  // owned layers below this one: owned layers alternate buffers
+    for (int j = 0; j < tid; j++) nown += c < net.ly[j].P;
+    g_rb[tid] = (nown & 1) * kWarps * 32;
   }
   // Owned output columns: those of the CTA's last-hidden rows (all inputs
   // when there is no hidden layer; then the launch has one CTA).
@@ -101,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int l = 0; l < H; l++) {  // smem-resident hidden layers: load the rows once
     const LayerDev& ly = net.ly[l];
-    if (ly.res != kResSmem) continue;
+    if (!(FEAT & kFeatSmem) || ly.res != kResSmem) continue;
     const float4* g = reinterpret_cast<const float4*>(ly.w + (size_t)g_r0[l] * ly.pitch);
     float4* s = reinterpret_cast<float4*>(sm + ly.wsm_off);
     for (int i = tid; i < g_nr[l] * ly.pitch / 4; i += kThreads) s[i] = g[i];
@@ -200,16 +212,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (mine) {
           const SrcSlots sl{lp.yll + ((size_t)buf * lp.P << lp.ylog), lp.R, lp.ylog, ly.fi};
           if (ly.res == kResReg) gather_regcols<RC + RS>(sl, sm + ly.in_off, seq, net.err);
-          else gather_quads(sl, ly.pitch >> 2, ly.gs, sm + ly.in_off, seq, net.err);
+          else if (FEAT & (kFeatSmem | kFeatL2))
+            gather_quads(sl, ly.pitch >> 2, ly.gs, sm + ly.in_off, seq, net.err);
         }
         XE();
         PHL(4, l, 1);
         TRACE(2 + 2 * (l - 1));
       }
       if (mine) {
-        // consecutive layers alternate reduction buffers: no barrier is needed
-        // between this layer's writes and the previous layer's last reads
-        float* redl = red + (l & 1) * kWarps * 32;
+        // consecutive OWNED layers alternate reduction buffers: the barrier
+        // inside the forward of the owned layer between two users of one
+        // buffer orders the later writes after the earlier reads (a CTA may
+        // own layers l and l+2 but not l+1)
+        float* redl = red + g_rb[l];
         const float4* v4 = reinterpret_cast<const float4*>(l == 0 ? in0 : sm + ly.in_off);
         unsigned long long* ys =
             (l < H - 1) ? ly.yll + ((size_t)buf * ly.P << ly.ylog) + ((size_t)c << ly.ylog)
@@ -222,10 +237,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               reg_fwd<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.pitch, g_nr[l],
                                   reinterpret_cast<const float*>(v4), redl, sm + ly.t_off, yo,
                                   ys, seq);
-        } else if (ly.res == kResSmem)
+        } else if ((FEAT & kFeatSmem) && ly.res == kResSmem)
           fwd_dispatch<true>(reinterpret_cast<const float4*>(sm + ly.wsm_off), ly, g_nr[l], v4,
                              redl, sm + ly.t_off, yo, ys, seq, (prof && l == 0) ? ph + 14 : nullptr);
-        else
+        else if (FEAT & kFeatL2)
           fwd_dispatch<false>(reinterpret_cast<const float4*>(ly.w + (size_t)g_r0[l] * ly.pitch),
                               ly, g_nr[l], v4, redl, sm + ly.t_off, yo, ys, seq);
       }
@@ -321,17 +336,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < NRL; i++)
             if (net.reg_layer[i] == l)
               reg_partials<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.fi, g_nr[l], dl, ps, seq);
-        } else if (ly.res == kResSmem)
+        } else if ((FEAT & kFeatSmem) && ly.res == kResSmem)
           bwd_partials<true, false>(reinterpret_cast<float4*>(sm + ly.wsm_off), ly.pitch >> 2,
                                     ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
-        else
+        else if (FEAT & kFeatL2)
           bwd_partials<false, true>(
               reinterpret_cast<float4*>(ly.w + (size_t)g_r0[l] * ly.pitch), ly.pitch >> 2,
               ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
       }
       PHL(8, l, 2);
       TRACE(1 + 2 * (L - 1 + (H - 1 - l)));
-      if (mine && ly.res == kResSmem)
+      if ((FEAT & kFeatSmem) && mine && ly.res == kResSmem)
         update_rows<true>(reinterpret_cast<float4*>(sm + ly.wsm_off), ly.pitch >> 2, ly.gs,
                           g_nr[l], reinterpret_cast<const float4*>(sm + ly.in_off), sl);
       if (mine && ly.res == kResReg) {
@@ -371,10 +386,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (net.reg_layer[i] == 0)
             reg_update<RR, RC, RS>(wr[i], sm + l0.wsm_off, l0.pitch, g_nr[0], in0,
                                    sm + net.dsc_off[cur]);
-      } else if (l0.res == kResSmem)
+      } else if ((FEAT & kFeatSmem) && l0.res == kResSmem)
         update_rows<true>(reinterpret_cast<float4*>(sm + l0.wsm_off), l0.pitch >> 2, l0.gs,
                           g_nr[0], x4, sm + net.dsc_off[cur]);
-      else
+      else if (FEAT & kFeatL2)
         update_rows<false>(reinterpret_cast<float4*>(l0.w + (size_t)g_r0[0] * l0.pitch),
                            l0.pitch >> 2, l0.gs, g_nr[0], x4, sm + net.dsc_off[cur]);
     }
@@ -395,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int l = 0; l < H; l++) {  // write the resident rows back
     const LayerDev& ly = net.ly[l];
-    if (ly.res != kResSmem) continue;
+    if (!(FEAT & kFeatSmem) || ly.res != kResSmem) continue;
     float4* g = reinterpret_cast<float4*>(ly.w + (size_t)g_r0[l] * ly.pitch);
     const float4* s = reinterpret_cast<const float4*>(sm + ly.wsm_off);
     for (int i = tid; i < g_nr[l] * ly.pitch / 4; i += kThreads) g[i] = s[i];
@@ -423,41 +438,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (counter && wrong_out != nullptr) atomicAdd(wrong_out, s_wrong);
 }
 
-// The compiled register plans: none; one 14-row block of 4 register column
-// slots + 1 shared-memory slot (the 2000x2501 hidden layer of C4: 14 rows x
-// 2504 columns per CTA); and up to four 7-row x 2-column blocks (1000-wide
-// layers: C5).
-#define DMLP_VARIANT(n, rr, rc, rs)                                            \
-  {n, rr, rc, rs, (const void*)k_train<n, rr, rc, rs, false>,                  \
-   (const void*)k_train<n, rr, rc, rs, true>}
-static const TrainVariant kVariants[] = {
-    DMLP_VARIANT(0, 1, 1, 0), DMLP_VARIANT(1, 14, 4, 1), DMLP_VARIANT(2, 7, 2, 0),
-    DMLP_VARIANT(4, 7, 2, 0), DMLP_VARIANT(3, 8, 2, 0),
-};
-#undef DMLP_VARIANT
-
-int train_variants(const TrainVariant** out) {
-  *out = kVariants;
-  return (int)(sizeof(kVariants) / sizeof(kVariants[0]));
-}
-
-cudaError_t set_train_attributes(const void* fn, int smem_bytes) {
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-}
-
-cudaError_t train_occupancy(const void* fn, int smem_bytes, int* blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads, smem_bytes);
-}
-
-cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
-                         const uint8_t* labels, const int32_t* order, long long n, float eta,
-                         uint32_t seq0, long long* wrong, float* y_last, cudaStream_t st) {
-  NetDev nd = net->dev;
-  unsigned long long* w = reinterpret_cast<unsigned long long*>(wrong);
-  void* args[] = {&nd, &x, &ldx, &labels, &order, &n, &eta, &seq0, &w, &y_last};
-  const void* fn = (nd.prof || nd.trace) ? net->train_fn_prof : net->train_fn;
-  return cudaLaunchCooperativeKernel(fn, dim3(nd.nct), dim3(kThreads), args,
-                                     (size_t)net->smem_bytes, st);
-}
+// The compiled register plans (NRL, RR, RC, RS): none; one 14-row block of
+// 4 register column slots + 1 shared-memory slot (the 2000x2501 hidden layer
+// of C4: 14 rows x 2504 columns per CTA); up to four 7-row x 2-column blocks
+// and three 8-row x 2-column blocks (1000-wide layers: C5, C1).
+#define DMLP_REGISTER_PLANS(X) X(0, 1, 1, 0) X(1, 14, 4, 1) X(2, 7, 2, 0) X(4, 7, 2, 0) X(3, 8, 2, 0)
+constexpr int kNumPlans = 5;
 
 }  // namespace dmlp

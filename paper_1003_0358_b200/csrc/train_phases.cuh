@@ -22,7 +22,16 @@ __device__ __forceinline__ void st_flag(unsigned long long* p, float x, uint32_t
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __noinline__ void spin_fail(int* err) {
+// CTA barrier after per-thread spin loops.  bar.sync is the .aligned form:
+// every lane of a warp must arrive at it together, and the lanes leave a
+// poll loop in different rounds; ptxas does not always reconverge them
+// before the barrier (seen as wrong results in the register-only instance,
+// flagged by compute-sanitizer --tool synccheck), so reconverge explicitly.
+__device__ __forceinline__ void cta_sync() {
+  asm volatile("barrier.sync 0;" ::: "memory");
+}
+
+static __device__ __noinline__ void spin_fail(int* err) {
   atomicExch(err, 1);
   __trap();
 }
@@ -170,7 +179,7 @@ __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, 
     }
     const float s = xpose_reduce<CH>(acc, lane);
     if ((lane & (32 / CH - 1)) == 0) red[warp * CH + lane / (32 / CH)] = s;
-    __syncthreads();
+    cta_sync();
     SUBP(0);
     if (tid < G * CH) {
       const int gg = tid / CH, jj = tid - gg * CH;
@@ -364,7 +373,7 @@ __device__ __forceinline__ void reg_fwd(const float (&w)[RR][RC], float* tail, i
   }
   const float s = xpose_reduce<CH>(acc, lane);
   if ((lane & (32 / CH - 1)) == 0) red[warp * CH + lane / (32 / CH)] = s;
-  __syncthreads();
+  cta_sync();
   if (tid < nr) {
     const float a = tree_sum<CH>(red + tid, kWarps);
     float t;
@@ -589,7 +598,7 @@ __device__ __forceinline__ void gather_sum(const unsigned long long* src, int st
         if (off[u] >= 0) acc += __uint_as_float((uint32_t)v[u]);
     }
     red[warp * 32 + lane] = acc;
-    __syncthreads();
+    cta_sync();
     if (tid < 32 && k0 + tid < nr) {
       fin(k0 + tid, tree_sum<32>(red + tid, kWarps));
     }

@@ -1,0 +1,58 @@
+"""compute-sanitizer checks of the persistent training kernel (B200).
+
+The flag-word exchanges leave the lanes of a warp in different poll rounds;
+the CTA barriers after them must tolerate that (train_phases.cuh cta_sync).
+synccheck catches a barrier reached by a divergent warp -- the failure that
+made the register-only instance compute wrong weights -- and racecheck the
+shared-memory hazards between the phases.  Each check runs a few samples of
+a small net in a subprocess, once per compiled feature instance (register
+rows only; smem + L2 paths forced in with DMLP_FEAT).
+"""
+
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from oracle import oracle as O
+from paper_1003_0358_b200.device import DeviceNet
+g = np.load(%r); x = g['deformed'].reshape(64, -1); lab = g['labels']
+sizes = tuple(int(v) for v in sys.argv[1].split(','))
+n = int(sys.argv[2])
+dn = DeviceNet(sizes); dn.set_layers(O.init_layers(7, sizes))
+wrong = torch.zeros((), dtype=torch.int64, device='cuda')
+dn.train_epoch(torch.from_numpy(x[:n]).cuda(), torch.from_numpy(lab[:n]).cuda(), None, 1e-3, wrong)
+torch.cuda.synchronize()
+print('ok', ''.join(r[0] for r in dn.layer_residency))
+""" % (ROOT, os.path.join(ROOT, "tests", "golden", "train.npz"))
+
+
+def _sanitizer():
+    for p in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if p and os.path.exists(p):
+            return p
+    pytest.skip("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["synccheck", "racecheck"])
+@pytest.mark.parametrize("feat", ["0", "3"])
+@pytest.mark.parametrize("sizes", ["841,300,120,10", "841,37,5,9,10"])
+def test_train_kernel_sanitizer(tmp_path, tool, feat, sizes):
+    script = tmp_path / "case.py"
+    script.write_text(CASE)
+    env = dict(os.environ, DMLP_FEAT=feat)
+    p = subprocess.run([_sanitizer(), "--tool", tool, "--print-limit", "4", "--error-exitcode", "9",
+                        sys.executable, str(script), sizes, "3"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0 and "ok " in out, out[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "0 hazards" in out, out[-3000:]
