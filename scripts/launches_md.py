@@ -23,8 +23,9 @@ out = ["# Round 1 launch list (ncu --metrics gpu__time_duration.sum --clock-cont
        "| kernel | launches | total ms | share |", "|---|---|---|---|"]
 for k, (n, ms) in agg.items():
     out.append(f"| `{k}` | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |")
-out += ["", "`k_train<NRL, RR, RC, RS>` is the persistent on-line BP kernel (the register plan "
-        "in the template arguments); one launch trains a whole step of samples. `k_gemm_tanh` + "
+out += ["", "`k_train<NRL, RR, RC, RS, FEAT, PROF>` is the persistent on-line BP kernel (register "
+        "plan; FEAT = residency paths compiled in, 1 smem + 2 L2; PROF = 1 is the profiling "
+        "instance the bench launches once for the per-phase profile); one launch trains a whole step of samples. `k_gemm_tanh` + "
         "`k_out_rank` are the validation/evaluation forward; `k_deform` the per-epoch "
         "deformation; `k_pack`/`k_unpack` the reference-layout conversions."]
 open('profiles/r1_launches.md', 'w').write("\n".join(out) + "\n")
