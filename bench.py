@@ -45,6 +45,7 @@ CONFIGS = {
     "C5": (841,) + (1000,) * 9 + (10,),
 }
 METRIC = "on-line BP train samples/s (bs=1, 12.11M MLP)"
+L2_BYTES = 126 * 1024 * 1024
 
 
 def count_weights(sizes) -> int:
@@ -358,8 +359,12 @@ def bench_config(args, world: int) -> dict:
                         f"{n} deformed synthetic digits per step",
             "weights": count_weights(sizes), "samples_per_step": n,
             "parallelism": "replicas only" if world > 1 else "single GPU",
-            "l2": "inputs larger than L2 (n*841*4 B per step); weights are deliberately "
-                  "kept on chip (smem / registers) or in L2"}
+            "input_bytes_per_step": n * 841 * 4,
+            "l2": (f"inputs larger than L2 ({n * 841 * 4 / 1e6:.0f} MB per step > 126 MB), "
+                   if n * 841 * 4 > L2_BYTES else
+                   f"inputs SMALLER than L2 ({n * 841 * 4 / 1e6:.0f} MB per step), ")
+                  + "each input row read once per step; weights are deliberately kept on chip "
+                    "(smem / registers) or in L2"}
 
 
 def l2_peak() -> float | None:
@@ -423,7 +428,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
-    ap.add_argument("--samples", type=int, default=20000, help="on-line samples per step")
+    ap.add_argument("--samples", type=int, default=40000,
+                    help="on-line samples per step (default: inputs > the 126 MB L2)")
     ap.add_argument("--deform-images", type=int, default=60000)
     ap.add_argument("--residency", default="auto")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -9,7 +9,7 @@ for c in ["c1", "c2", "c3", "c4", "c5"]:
                  d["cpu_baseline"]["value"], d["cpu_baseline"]["cores"],
                  "".join(w[0] for w in d["layer_residency"][:-1])))
 out = ["# Round 1 results (one B200, `python bench.py --config Cx`)", "",
-       "Value = on-line samples/s (bs=1) device-timed over 5 launches of 20,000 samples each, "
+       "Value = on-line samples/s (bs=1) device-timed over 5 launches of " f"{json.load(open('profiles/r1_bench_c4.json'))['config']['samples_per_step']:,} samples each, "
        "inputs resident in HBM; e2e = `trainer.train_epoch` from pinned host buffers (H2D of the "
        "step's images inside the timed region). Roofline: 12 B per weight per sample against the "
        "measured HBM copy peak (MEASURED_PEAKS.json, 6551 GB/s) and the L2 read+write peak "
