@@ -258,3 +258,37 @@ def test_gradient_check_oracle_on_gpu(golden):
     worst = kernels.gradient_check(mlp, g["x"], int(g["digit"]), step=1e-5)
     ref = float(g["worst"])
     assert worst < 1e-6 and ref / 10 <= worst <= ref * 10, (worst, ref)
+
+
+@pytest.mark.parametrize("cfg", ["small", "C4", "C5"])
+def test_train_epoch_launch_split_bit_identical(golden, cfg):
+    """One launch over n samples equals n one-sample launches BIT FOR BIT:
+    the cross-sample machinery inside a launch (input prefetch one sample
+    ahead, parity-double-buffered exchange words, register / smem-resident
+    rows carried across samples) changes no arithmetic (smem-resident layer
+    0: small / C4; L2-streamed layer 0: C5)."""
+    import torch
+
+    sizes = {"small": (841, 300, 120, 10),
+             "C4": (841, 2500, 2000, 1500, 1000, 500, 10),
+             "C5": (841,) + (1000,) * 9 + (10,)}[cfg]
+    x, lab = _inputs(golden)
+    n = 12
+    base = O.init_layers(3, sizes)
+    xd = torch.from_numpy(x[:n].copy()).cuda()
+    ld = torch.from_numpy(lab[:n].copy()).cuda()
+    outs, wrongs = [], []
+    for split in (False, True):
+        dn = _net(sizes, [w.copy() for w in base])
+        wrong = torch.zeros((), dtype=torch.int64, device="cuda")
+        if split:
+            for i in range(n):
+                dn.train_epoch(xd[i:i + 1], ld[i:i + 1], None, 1e-3, wrong)
+        else:
+            dn.train_epoch(xd, ld, None, 1e-3, wrong)
+        torch.cuda.synchronize()
+        wrongs.append(int(wrong.item()))
+        outs.append(np.concatenate([w.ravel() for w in dn.get_layers()]))
+        dn.close()
+    assert wrongs[0] == wrongs[1]
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
