@@ -170,6 +170,10 @@ static void set_geometry(dmlp_net* net, int nct, size_t* yoff, size_t* poff, int
     if (rround > 1) ly.R = (ly.R + rround - 1) / rround * rround;
     ly.P = (ly.fo + ly.R - 1) / ly.R;
     ly.ylog = ceil_log2(ly.R < 16 ? 16 : ly.R);
+    // flat y words: a consumer's quad is then always one 32-byte pair of
+    // vector polls (per-producer slots only give that when R % 4 == 0)
+    ly.yflat = (ly.R & 3) != 0;
+    if (const char* yf = getenv("DMLP_YFLAT")) ly.yflat = atoi(yf) == 2 ? 1 : atoi(yf) == 0 ? 0 : ly.yflat;
     ly.pstride = round_up(ly.fi, 16);
     choose_mapping(ly);
     yoff[l] = ll;
@@ -184,6 +188,7 @@ static void set_geometry(dmlp_net* net, int nct, size_t* yoff, size_t* poff, int
     lo.R = H > 0 ? d.ly[H - 1].R : lo.fi;  // owned input columns per CTA
     lo.P = H > 0 ? d.ly[H - 1].P : 1;
     lo.ylog = ceil_log2(lo.fo < 16 ? 16 : lo.fo);
+    lo.yflat = 0;
     lo.gs = 0;
     lo.CH = 1;
     lo.pstride = 0;

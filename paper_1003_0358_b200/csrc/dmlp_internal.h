@@ -39,6 +39,8 @@ struct LayerDev {
   int P;                 // CTAs owning at least one row (output: producing a partial)
   int gs, CH;            // hidden: log2 of the row groups G, rows per reduction chunk
   int ylog;              // log2 words per producer slot of yll (>= 16 words, line aligned)
+  int yflat;             // hidden: y words stored flat (word of row i at i) instead of per
+                         // producer slot, so every float4 quad is 4 consecutive words
   int pstride;           // hidden l>=1: per-CTA row stride of pll (multiple of 16 words)
   float* w;              // [fo][pitch], reference order, bias in column fi
   // Exchange buffers: every CTA's slice starts on its own 128-byte line, so a

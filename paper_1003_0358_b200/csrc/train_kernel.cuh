@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const LayerDev& lp = net.ly[l - 1];
         XB();
         if (mine) {
-          const SrcSlots sl{lp.yll + ((size_t)buf * lp.P << lp.ylog), lp.R, lp.ylog, ly.fi};
+          const SrcSlots sl{lp.yll + ((size_t)buf * lp.P << lp.ylog), lp.R, lp.ylog, ly.fi,
+                           lp.yflat};
           if (ly.res == kResReg) gather_regcols<RC + RS>(sl, sm + ly.in_off, seq, net.err);
           else if (FEAT & (kFeatSmem | kFeatL2))
             gather_quads(sl, ly.pitch >> 2, ly.gs, sm + ly.in_off, seq, net.err);
@@ -227,7 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* redl = red + g_rb[l];
         const float4* v4 = reinterpret_cast<const float4*>(l == 0 ? in0 : sm + ly.in_off);
         unsigned long long* ys =
-            (l < H - 1) ? ly.yll + ((size_t)buf * ly.P << ly.ylog) + ((size_t)c << ly.ylog)
+            (l < H - 1) ? ly.yll + ((size_t)buf * ly.P << ly.ylog) +
+                              (ly.yflat ? (size_t)g_r0[l] : ((size_t)c << ly.ylog))
                         : nullptr;
         float* yo = (l == H - 1) ? sm + net.yown_off : nullptr;
         if (ly.res == kResReg) {

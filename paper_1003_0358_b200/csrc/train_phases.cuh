@@ -467,6 +467,7 @@ constexpr int kGatherU = 10;  // producer lines per warp per batch (16 warps x 1
 struct SrcSlots {
   const unsigned long long* src;  // this sample's [P][2^ylog] slots of the producing layer
   int R, ylog, fi;                // producer rows, slot stride (log2 words), consumer fan-in
+  int flat;                       // word of column i at src[i] (LayerDev::yflat)
 };
 
 template <int U>
@@ -478,7 +479,7 @@ __device__ __forceinline__ void gather_cols(const SrcSlots& sl, const int (&col)
     const int i = col[j];
     if (i >= 0 && i < sl.fi) {
       const int p = i / sl.R;
-      off[j] = (p << sl.ylog) + (i - p * sl.R);
+      off[j] = sl.flat ? i : (p << sl.ylog) + (i - p * sl.R);
     } else {
       off[j] = -1;
     }
@@ -496,6 +497,11 @@ __device__ __forceinline__ void gather_cols(const SrcSlots& sl, const int (&col)
 // carry.
 __device__ __forceinline__ void quad_offsets(const SrcSlots& sl, int q, int (&off)[4]) {
   const int i0 = 4 * q;
+  if (sl.flat) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) off[j] = (i0 + j < sl.fi) ? i0 + j : -1;
+    return;
+  }
   int p = i0 / sl.R, r = i0 - p * sl.R;
 #pragma unroll
   for (int j = 0; j < 4; j++) {
@@ -509,11 +515,12 @@ __device__ __forceinline__ void gather_quads(const SrcSlots& sl, int nq, int gs,
   const int TG = kThreads >> gs, u = threadIdx.x & (TG - 1);
   if (nq <= TG) {
     if (u >= nq) return;
-    if ((sl.R & 3) == 0 && 4 * u + 4 <= sl.fi) {
-      // producer blocks of a multiple of 4 rows: the quad is 4 consecutive,
-      // 32-byte aligned words of one producer's slot -> two vector polls
+    if ((sl.flat || (sl.R & 3) == 0) && 4 * u + 4 <= sl.fi) {
+      // flat words, or producer blocks of a multiple of 4 rows: the quad is
+      // 4 consecutive, 32-byte aligned words -> two vector polls
       const int p = 4 * u / sl.R;
-      const unsigned long long* a = sl.src + (p << sl.ylog) + (4 * u - p * sl.R);
+      const unsigned long long* a =
+          sl.src + (sl.flat ? 4 * u : (p << sl.ylog) + (4 * u - p * sl.R));
       unsigned long long w0, w1, w2, w3;
       long long t0 = 0;
       for (int round = 0;; round++) {
