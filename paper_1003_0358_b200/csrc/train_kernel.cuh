@@ -250,6 +250,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (l < H - 1) TRACE(1 + 2 * l);
     }
 
+    // np.argmax of the output (first maximum; NaN counts as maximum) by one
+    // thread of CTA 0.  (Deferring it past the first backward publish or to
+    // the end of the sample measured slower: scripts/ab_perf.sh.)
+    auto count_error = [&]() {
+      if (counter) {
+        int best = 0;
+        float bv = outv[kMaxOut];
+        for (int k = 1; k < lo.fo && !(bv != bv); k++) {
+          const float yk = outv[kMaxOut + k];
+          if (yk > bv || yk != yk) { bv = yk; best = k; }
+        }
+        s_wrong += (best != digit);
+      }
+    };
+
     // ---------------- output layer: partials of the owned columns ----------------
     const float* yin = H > 0 ? sm + net.yown_off : in0;
     __syncthreads();
@@ -263,34 +278,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     PH(5);
     TRACE(1 + 2 * (L - 2));
     XB();
+    // the output activation and delta are formed by the thread that finishes
+    // the sum (gather_sum's closing barrier publishes them to the CTA)
     if (oown)
       gather_sum(lo.yll + ((size_t)buf * lo.P << lo.ylog), 1 << lo.ylog, lo.P, 0, lo.fo, red, seq,
-                 net.err, [&](int k, float a) { outv[k] = a; });
+                 net.err, [&](int k, float a) {
+                   float t;
+                   const float y = tanh_scaled_noinline(a, &t);
+                   const float d = dev_output_delta_t(y, t, k == digit ? 1.0f : -1.0f);
+                   outv[k] = a;
+                   outv[kMaxOut + k] = y;
+                   outv[2 * kMaxOut + k] = d;
+                   outv[3 * kMaxOut + k] = __fmul_rn(eta, d);
+                 });
     else
       __syncthreads();
     XE();
     PH(6);
     TRACE(2 + 2 * (L - 2));
     if (oown) {
-      if (tid < lo.fo) {
-        const float a = outv[tid];
-        float t;
-        const float y = tanh_scaled_noinline(a, &t);
-        const float d = dev_output_delta_t(y, t, tid == digit ? 1.0f : -1.0f);
-        outv[kMaxOut + tid] = y;
-        outv[2 * kMaxOut + tid] = d;
-        outv[3 * kMaxOut + tid] = __fmul_rn(eta, d);
-      }
-      __syncthreads();
-      if (counter) {  // np.argmax: first maximum (NaN counts as maximum)
-        int best = 0;
-        float bv = outv[kMaxOut];
-        for (int k = 1; k < lo.fo && !(bv != bv); k++) {
-          const float yk = outv[kMaxOut + k];
-          if (yk > bv || yk != yk) { bv = yk; best = k; }
-        }
-        s_wrong += (best != digit);
-      }
+      count_error();
       if (c == 0 && s == n - 1 && y_last != nullptr && tid < lo.fo)
         y_last[tid] = outv[kMaxOut + tid];
       // Deltas of the owned last-hidden rows through the OLD output weights,
