@@ -12,7 +12,7 @@ out = ["# Round 1 results (one B200, `python bench.py --config Cx`)", "",
        "Value = on-line samples/s (bs=1) device-timed over 5 launches of " f"{json.load(open('profiles/r1_bench_c4.json'))['config']['samples_per_step']:,} samples each, "
        "inputs resident in HBM; e2e = `trainer.train_epoch` from pinned host buffers (H2D of the "
        "step's images inside the timed region). Roofline: 12 B per weight per sample against the "
-       "measured HBM copy peak (MEASURED_PEAKS.json, 6551 GB/s) and the L2 read+write peak "
+       "measured HBM copy peak (MEASURED_PEAKS.json, " f"{json.load(open('profiles/r1_bench_c4.json'))['roofline']['peak']:.0f} GB/s) and the L2 read+write peak "
        "measured in the same run. CPU = the reference algorithm (oracle port, bit-exact with the "
        "reference tiled variant) on the box's host cores. Layer residency per hidden layer: "
        "s = shared memory, r = register row block, l = streamed from L2.", "",
