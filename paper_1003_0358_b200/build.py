@@ -23,6 +23,8 @@ BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+# experiments: extra nvcc flags for A/B variant builds (e.g. "-DDMLP_BWD_ST4=1")
+COMMON += os.environ.get("DMLP_NVCC_FLAGS", "").split()
 UNITS = {
     "capi.cu": [],
     "train_inst_f0.cu": [],

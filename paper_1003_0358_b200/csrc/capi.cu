@@ -134,23 +134,26 @@ static long long resident_floats(const NetDev& d, unsigned mask) {
 // count G = 2^gs minimising the serial steps ceil(R/G) * ceil(quads/(512/G))
 // (plus reduction chunks), and the reduction chunk CH >= rows per group
 // (capped at 16: chunks beyond).
-static void choose_mapping(LayerDev& ly) {
+static void choose_mapping(LayerDev& ly, bool stages, int force_gs) {
   const int nq = ly.pitch / 4;
   int best = 1 << 30;
   for (int gs = 0; (1 << gs) <= kWarps; gs++) {
     const int G = 1 << gs, TG = kThreads / G;
     const int C = (nq + TG - 1) / TG, nj = (ly.R + G - 1) / G;
     // G > 1 stages G partial vectors in smem for the backward pass: only for
-    // narrow layers, where the staging costs little shared memory
-    if (G > 1 && G * ly.pitch > 2048) break;
+    // narrow layers, where the staging costs little shared memory (layer 0
+    // has no backward pass and stages nothing)
+    if (stages && G > 1 && G * ly.pitch > 2048) break;
     // G > 1 also costs a duplicated input gather and (backward) a staged
-    // combine of the partials: only worth it for a clear win
-    const int cost = C * nj + (G > 1 ? 4 : 0) + 8 * ((nj + 15) / 16 - 1);
+    // combine of the partials: only worth it for a clear win (layer 0 has
+    // neither: C5's layer 0 with G = 2 instead of 1 is +0.8%, scripts/gs_ab.sh)
+    const int cost = C * nj + (stages && G > 1 ? 4 : 0) + 8 * ((nj + 15) / 16 - 1);
     if (cost < best) {
       best = cost;
       ly.gs = gs;
     }
   }
+  if (force_gs >= 0 && (1 << force_gs) <= kWarps) ly.gs = force_gs;
   const int nj = (ly.R + (1 << ly.gs) - 1) >> ly.gs;
   ly.CH = nj <= 4 ? 4 : nj <= 8 ? 8 : 16;
 }
@@ -175,7 +178,12 @@ static void set_geometry(dmlp_net* net, int nct, size_t* yoff, size_t* poff, int
     ly.yflat = (ly.R & 3) != 0;
     if (const char* yf = getenv("DMLP_YFLAT")) ly.yflat = atoi(yf) == 2 ? 1 : atoi(yf) == 0 ? 0 : ly.yflat;
     ly.pstride = round_up(ly.fi, 16);
-    choose_mapping(ly);
+    int force_gs = -1;  // experiments: DMLP_GS="gs0,gs1,..." per hidden layer, -1 = auto
+    if (const char* g = getenv("DMLP_GS")) {
+      for (int i = 0; i < l && g; i++) g = strchr(g, ',') ? strchr(g, ',') + 1 : nullptr;
+      if (g) force_gs = atoi(g);
+    }
+    choose_mapping(ly, l >= 1, force_gs);
     yoff[l] = ll;
     if (l < H - 1) ll += 2 * (size_t)ly.P << ly.ylog;
     if (l >= 1) {

@@ -5,7 +5,7 @@ CSRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_100
 for unit in sys.argv[1:]:
     r = subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
                         "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas",
-                        "-v", "-c", f"{unit}.cu", "-o", f"/tmp/{unit}.o"],
+                        "-v", *os.environ.get("DMLP_NVCC_FLAGS", "").split(), "-c", f"{unit}.cu", "-o", f"/tmp/{unit}.o"],
                        cwd=CSRC, capture_output=True, text=True)
     name = None
     for line in r.stderr.splitlines():
