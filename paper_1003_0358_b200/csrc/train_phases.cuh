@@ -229,6 +229,32 @@ __device__ __forceinline__ void bwd_partials(float4* W4, int nq, int fi, int gs,
     const float4 x = FUSE ? v4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     float4* Wq = W4 + mp.g * nq + q;
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (FUSE && mp.nj <= 8) {
+      // streamed layer: every owned row's weights in flight at once (one L2
+      // round trip), the partials published before the update's stores
+      float4 w[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        w[i] = i < mp.nj ? ldw4<RES>(Wq + i * rstep) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        if (i < mp.nj) {
+          const float d = delta[mp.g + (i << gs)];
+          p.x = fmaf(w[i].x, d, p.x);
+          p.y = fmaf(w[i].y, d, p.y);
+          p.z = fmaf(w[i].z, d, p.z);
+          p.w = fmaf(w[i].w, d, p.w);
+        }
+      }
+      if (4 * q < fi) {
+        if (gs == 0) st_flag4(pslot + 4 * q, p, fi - 4 * q, seq);
+        else reinterpret_cast<float4*>(pbuf)[mp.g * nq + q] = p;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if (i < mp.nj) stw4<RES>(Wq + i * rstep, upd4(w[i], dsc[mp.g + (i << gs)], x));
+      continue;
+    }
     int j = 0;
     for (; j + 4 <= mp.nj; j += 4) {
       float4 w[4];
