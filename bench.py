@@ -325,6 +325,7 @@ def run_gpu(args) -> dict | None:
         "residency": dn.residency,
         "l2_peak_rw_GBs": l2, "frac_of_l2_rw": round(achieved / l2, 4) if l2 else None,
         "exchange_fraction": round(prof["exchange_fraction"], 3),
+        "sync_bound": sync_bound(len(sizes) - 1, sps_rank),
     }
     cpu = cpu_train_rate(sizes, seconds=args.cpu_seconds) if args.cpu_seconds > 0 else None
     line = {
@@ -376,6 +377,27 @@ def l2_peak() -> float | None:
         return round(2 * (48 << 20) * 10 / s / 1e9, 1)
     except Exception:
         return None
+
+
+def sync_bound(n_layers: int, sps: float) -> dict | None:
+    """SURVEY.md §8(d) sync bound: the 2L-3 all-to-all exchanges a sample
+    needs (forward y of hidden layers 0..H-2, output partials, backward
+    partials of layers H-1..1), each at the measured floor of a bare
+    148-CTA exchange (K6 protocol E, the kernel's poll discipline)."""
+    try:
+        from paper_1003_0358_b200 import microbench
+
+        rounds = 3000
+        s, cyc = microbench.run(5, 4 | (16 << 8), rounds, 148)
+    except Exception:
+        return None
+    hops = max(2 * n_layers - 3, 0)
+    hop_us = s / rounds * 1e6
+    us = hops * hop_us
+    return {"exchanges_per_sample": hops, "hop_us": round(hop_us, 3),
+            "hop_cycles": round(cyc / rounds, 1), "us_per_sample": round(us, 2),
+            "samples_per_s": round(1e6 / us, 1) if us > 0 else None,
+            "share_of_measured_sample": round(us * sps / 1e6, 3)}
 
 
 def profiled_traffic(cfg: str, samples: int):
