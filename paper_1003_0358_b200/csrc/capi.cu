@@ -144,6 +144,10 @@ static void choose_mapping(LayerDev& ly, bool stages, int force_gs) {
     // narrow layers, where the staging costs little shared memory (layer 0
     // has no backward pass and stages nothing)
     if (stages && G > 1 && G * ly.pitch > 2048) break;
+    // without that limit (layer 0) the count model would trade rows for
+    // quads down to one row per 32-thread group (C3: gs = 4, -4.8%): keep
+    // one quad per thread
+    if (!stages && G > 1 && C > 1) break;
     // G > 1 also costs a duplicated input gather and (backward) a staged
     // combine of the partials: only worth it for a clear win (layer 0 has
     // neither: C5's layer 0 with G = 2 instead of 1 is +0.8%, scripts/gs_ab.sh)
