@@ -45,6 +45,13 @@
 namespace dmlp {
 
 constexpr int kProfSlots = kProfWords;
+// gather_sum lane groups per register plan (compile time: selecting at run
+// time cost C4 ~4%): halves for <= 16 rows (C4 36.3k -> 37.4k samples/s, C5
+// +3.6%), quarters for <= 8 rows with the 1000-wide plans (C1, C5), none
+// without register rows (C2: halves -2.2%)
+#ifndef DMLP_GATHER_SPLIT
+#define DMLP_GATHER_SPLIT(NRL, RR) ((NRL) == 0 ? 1 : (RR) <= 8 ? 4 : 2)
+#endif
 // FEAT: which residency paths are compiled in (kFeatSmem: shared-memory
 // hidden layers, kFeatL2: L2-streamed ones; register row blocks always):
 // code a net never runs still costs registers and instruction fetch in the
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the output activation and delta are formed by the thread that finishes
     // the sum (gather_sum's closing barrier publishes them to the CTA)
     if (oown)
-      gather_sum(lo.yll + ((size_t)buf * lo.P << lo.ylog), 1 << lo.ylog, lo.P, 0, lo.fo, red, seq,
+      gather_sum<DMLP_GATHER_SPLIT(NRL, RR)>(lo.yll + ((size_t)buf * lo.P << lo.ylog), 1 << lo.ylog, lo.P, 0, lo.fo, red, seq,
                  net.err, [&](int k, float a) {
                    float t;
                    const float y = tanh_scaled_noinline(a, &t);
@@ -373,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* tcb = sm + lb.t_off;
       XB();
       if (c < lb.P)
-        gather_sum(pb, ly.pstride, ly.P, g_r0[l - 1], g_nr[l - 1], red, seq, net.err,
+        gather_sum<DMLP_GATHER_SPLIT(NRL, RR)>(pb, ly.pstride, ly.P, g_r0[l - 1], g_nr[l - 1], red, seq, net.err,
                    [&](int k, float a) {
                      const float d = dev_hidden_delta(a, tcb[k]);
                      dn[k] = d;

@@ -481,13 +481,6 @@ __device__ __forceinline__ void poll_batch(const unsigned long long* base, const
   }
 }
 
-// gather_sum with half-warps on alternate producers for <= 16 rows: C4
-// 36.3k -> 37.4k samples/s, C5 +3.6%, C3 +0.7%, C1 +0.3%, C2 -2.2%
-// (scripts/ab_perf.sh).  Compile-time on purpose: selecting it at run time
-// (both forms compiled into the kernel) cost C4 ~4%.
-#ifndef DMLP_GATHER_SPLIT
-#define DMLP_GATHER_SPLIT 1
-#endif
 constexpr int kGatherU = 10;  // producer lines per warp per batch (16 warps x 10 >= 148)
 
 // ---- own-column gather (forward) ---------------------------------------------
@@ -611,41 +604,56 @@ __device__ __forceinline__ void gather_regcols(const SrcSlots& sl, float* v, uin
   gather_cols<NC>(sl, col, v, seq, err);
 }
 
+// gather_sum for nr <= 32 / S rows: the S lane groups of a warp take
+// alternate producers (group h of warp w sums producers w + 16h,
+// w + 16h + 16S, ...), so a lane keeps 1/S as many polls in flight; the
+// groups are then combined by a fixed butterfly (deterministic).
+template <int S, class Fin>
+__device__ __forceinline__ void gather_sum_split(const unsigned long long* src, int stride, int P,
+                                                 int o, int nr, float* red, uint32_t seq,
+                                                 int* err, Fin fin) {
+  constexpr int W = 32 / S;                                   // lanes per group = max rows
+  constexpr int U = (16 * kGatherU + 16 * S - 1) / (16 * S);  // >= 160 producers per batch
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = lane / W, k = lane % W;
+  const bool kv = k < nr;
+  float acc = 0.0f;
+  for (int pb = 0; pb < P; pb += S * kWarps * U) {
+    int off[U];
+    unsigned long long v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int p = pb + warp + kWarps * (S * u + h);
+      off[u] = (kv && p < P) ? p * stride + o + k : -1;
+    }
+    poll_batch<U>(src, off, v, seq, err);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (off[u] >= 0) acc += __uint_as_float((uint32_t)v[u]);
+  }
+#pragma unroll
+  for (int m = 16; m >= W; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (h == 0) red[warp * 32 + k] = acc;
+  cta_sync();
+  if (tid < nr) fin(tid, tree_sum<32>(red + tid, kWarps));
+  __syncthreads();
+}
+
 // s_k = sum over producers c < P of src[c*stride + o + k], k < nr, in a
 // fixed order (producers c = w + 16*i summed by warp w in ascending i, then
 // the 16 warp sums in ascending w): deterministic, independent of timing,
 // no staging buffer.  fin(k, s_k) runs on one thread per k.
-template <class Fin>
+template <int SPLIT = 1, class Fin>
 __device__ __forceinline__ void gather_sum(const unsigned long long* src, int stride, int P,
                                            int o, int nr, float* red, uint32_t seq, int* err,
                                            Fin fin) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (DMLP_GATHER_SPLIT && nr <= 16) {
-    // at most 16 rows: the two half-warps take alternate producers (half h
-    // of warp w sums producers w + 16h, w + 16h + 32, ...), so a lane keeps
-    // half as many polls in flight; then one fixed pairing of the halves
-    constexpr int U = kGatherU / 2;
-    const int h = lane >> 4, k = lane & 15;
-    const bool kv = k < nr;
-    float acc = 0.0f;
-    for (int pb = 0; pb < P; pb += 2 * kWarps * U) {
-      int off[U];
-      unsigned long long v[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int p = pb + warp + kWarps * (2 * u + h);
-        off[u] = (kv && p < P) ? p * stride + o + k : -1;
-      }
-      poll_batch<U>(src, off, v, seq, err);
-#pragma unroll
-      for (int u = 0; u < U; u++)
-        if (off[u] >= 0) acc += __uint_as_float((uint32_t)v[u]);
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-    if (h == 0) red[warp * 32 + k] = acc;
-    cta_sync();
-    if (tid < nr) fin(tid, tree_sum<32>(red + tid, kWarps));
-    __syncthreads();
+  if (SPLIT >= 4 && nr <= 8) {
+    gather_sum_split<4>(src, stride, P, o, nr, red, seq, err, fin);
+    return;
+  }
+  if (SPLIT >= 2 && nr <= 16) {
+    gather_sum_split<2>(src, stride, P, o, nr, red, seq, err, fin);
     return;
   }
   for (int k0 = 0; k0 < nr; k0 += 32) {
