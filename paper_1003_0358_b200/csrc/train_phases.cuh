@@ -639,6 +639,55 @@ __device__ __forceinline__ void gather_sum_split(const unsigned long long* src, 
   __syncthreads();
 }
 
+// gather_sum for 16 < nr <= 32 rows: one warp per producer would leave
+// 32 - nr lanes idle and give every lane ceil(P/16) polls (C4's 17 layer-0
+// rows: 10).  Instead the CTA is cut into G = 512/nr packed groups of nr
+// threads (17 rows: 30 groups, <= 5 polls per thread); group g sums
+// producers g, g + G, ... in ascending order, then one thread per row adds
+// the G group sums by a fixed pairwise tree (deterministic).  Measured and
+// off by default (scripts/ab_perf.sh, same box): C4 37.4k -> 35.1k samples/s,
+// C2 79.3k -> 78.9k, C1 +1%; build with -DDMLP_GATHER_PACK=1 to A/B it.
+#ifndef DMLP_GATHER_PACK
+#define DMLP_GATHER_PACK 0
+#endif
+template <class Fin>
+__device__ __forceinline__ void gather_sum_packed(const unsigned long long* src, int stride, int P,
+                                                  int o, int nr, float* red, uint32_t seq,
+                                                  int* err, Fin fin) {
+  constexpr int U = kGatherU;  // G >= 16 groups x 10 >= 160 producers per batch
+  const int tid = threadIdx.x;
+  const int G = kThreads / nr;
+  const int g = tid / nr, k = tid - g * nr;
+  const bool gv = g < G;
+  float acc = 0.0f;
+  for (int pb = 0; pb < P; pb += G * U) {
+    int off[U];
+    unsigned long long v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int p = pb + g + G * u;
+      off[u] = (gv && p < P) ? p * stride + o + k : -1;
+    }
+    poll_batch<U>(src, off, v, seq, err);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (off[u] >= 0) acc += __uint_as_float((uint32_t)v[u]);
+  }
+  if (gv) red[g * nr + k] = acc;
+  cta_sync();
+  if (tid < nr) {
+    float r[32];
+#pragma unroll
+    for (int i = 0; i < 32; i++) r[i] = i < G ? red[i * nr + tid] : 0.0f;
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1)
+#pragma unroll
+      for (int i = 0; i < h; i++) r[i] += r[i + h];
+    fin(tid, r[0]);
+  }
+  __syncthreads();
+}
+
 // s_k = sum over producers c < P of src[c*stride + o + k], k < nr, in a
 // fixed order (producers c = w + 16*i summed by warp w in ascending i, then
 // the 16 warp sums in ascending w): deterministic, independent of timing,
@@ -654,6 +703,10 @@ __device__ __forceinline__ void gather_sum(const unsigned long long* src, int st
   }
   if (SPLIT >= 2 && nr <= 16) {
     gather_sum_split<2>(src, stride, P, o, nr, red, seq, err, fin);
+    return;
+  }
+  if (DMLP_GATHER_PACK && nr > 16 && nr <= 32) {
+    gather_sum_packed(src, stride, P, o, nr, red, seq, err, fin);
     return;
   }
   for (int k0 = 0; k0 < nr; k0 += 32) {
