@@ -292,3 +292,39 @@ def test_train_epoch_launch_split_bit_identical(golden, cfg):
         dn.close()
     assert wrongs[0] == wrongs[1]
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+@pytest.mark.parametrize("ldx", [844, 900, 1683])
+def test_train_epoch_strided_rows_bit_identical(golden, ldx):
+    """dmlp_train_epoch's row stride (include/dmlp.h): rows read from a
+    padded (n, ldx) buffer through a column view give bit-identical weights
+    and error counts to the contiguous (n, 841) layout; an empty order is a
+    no-op; a stride below the fan-in is the reference's SizeMismatch."""
+    import torch
+
+    from paper_1003_0358_b200.errors import SizeMismatch
+
+    x, lab = _inputs(golden)
+    sizes = (841, 300, 120, 10)
+    base = O.init_layers(5, sizes)
+    perm = O.substream(0, 3, 1).permutation(64)
+    ld = torch.from_numpy(lab).cuda()
+    od = torch.from_numpy(perm.astype(np.int32)).cuda()
+    pad = torch.full((64, ldx), float("nan"), device="cuda")
+    pad[:, :841] = torch.from_numpy(x).cuda()
+    outs, wrongs = [], []
+    for xd in (torch.from_numpy(x).cuda(), pad[:, :841]):
+        dn = _net(sizes, [w.copy() for w in base])
+        wrong = torch.zeros((), dtype=torch.int64, device="cuda")
+        dn.train_epoch(xd, ld, od[:0], 1e-3, wrong)  # empty order: no sample
+        dn.train_epoch(xd, ld, od, 1e-3, wrong)
+        torch.cuda.synchronize()
+        wrongs.append(int(wrong.item()))
+        outs.append(np.concatenate([w.ravel() for w in dn.get_layers()]))
+        if xd.stride(0) != 841:
+            with pytest.raises(SizeMismatch):
+                dn.train_epoch(pad.view(-1)[:64 * 840].view(64, 840), ld, od, 1e-3, wrong)
+        dn.close()
+    assert wrongs[0] == wrongs[1]
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    assert np.isfinite(outs[1]).all()  # the NaN padding was never read
