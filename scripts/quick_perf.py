@@ -11,7 +11,8 @@ CONFIGS = {
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 res = sys.argv[2] if len(sys.argv) > 2 else "auto"
 names = sys.argv[3].split(",") if len(sys.argv) > 3 else list(CONFIGS)
-x = torch.rand((n, 841), device="cuda") * 2 - 1
+LDX = int(__import__("os").environ.get("LDX", "841"))  # row stride of the inputs
+x = (torch.rand((n, LDX), device="cuda") * 2 - 1)[:, :841]
 lab = torch.randint(0, 10, (n,), device="cuda", dtype=torch.uint8)
 for name in names:
     sizes = CONFIGS[name]
