@@ -31,11 +31,13 @@ extern "C" {
 
 /* Weight residency of the persistent training kernel. */
 #define DMLP_RES_AUTO 0   /* keep the largest set of layers that fits in smem, stream the rest */
-#define DMLP_RES_L2 1     /* weights in HBM, L2-persisting window, streamed every sample */
+#define DMLP_RES_L2 1     /* every hidden layer streamed through L2 (.cg) every sample */
 #define DMLP_RES_SMEM 2   /* every CTA keeps its owned rows in shared memory */
 #define DMLP_RES_HYBRID 3 /* (reported only) some layers resident, the rest streamed */
 #define DMLP_RES_MASK 0x10000 /* DMLP_RES_MASK | m: exactly the layers in bitmask m resident */
 #define DMLP_RES_NOREG 0x20000 /* with AUTO: shared memory / L2 only, no register row blocks */
+#define DMLP_RES_ALLPATHS 0x40000 /* run the kernel instance with every residency path compiled in
+                                     (same plan; for compute-sanitizer coverage) */
 
 typedef struct dmlp_net dmlp_net;
 
@@ -105,10 +107,12 @@ int dmlp_train_step(dmlp_net *net, const float *x, int32_t digit, float eta, flo
  * samples order[0..n) (order NULL = identity) of x_dev (rows of n_inputs
  * floats, row stride ldx floats) with labels_dev (u8).  Adds the number of
  * argmax errors to *wrong_dev (device int64).  y_last_dev (optional, 10
- * floats) receives the output of the last sample.  Asynchronous on stream. */
+ * floats) receives the output of the last sample.  pred_dev (optional, n
+ * bytes) receives the argmax of every sample's output in training order
+ * (np.argmax, first maximum: trainer.py:121).  Asynchronous on stream. */
 int dmlp_train_epoch(dmlp_net *net, const float *x_dev, int64_t ldx, const uint8_t *labels_dev,
                      const int32_t *order_dev, int64_t n, float eta, int64_t *wrong_dev,
-                     float *y_last_dev, void *stream);
+                     float *y_last_dev, uint8_t *pred_dev, void *stream);
 
 /* ---- evaluation (network.forward_batch / eval_report.evaluate) ---- */
 

@@ -438,6 +438,22 @@ void or_fp_naive(const float *w, int fo, int fi, const float *x, float *a, float
   }
 }
 
+/* kernels.py:74-83 _bp_naive: acc = delta_up[i] (zero) + sum over j in
+ * ascending order of w_ji * delta_j (mul then add), then the f64 derivative
+ * product exactly as the tiled reduce (numba promotes 1 - t*t to f64). */
+void or_bp_naive(const float *w, int fo, int fi, const float *dd, const float *a_up,
+                 float *du) {
+  const int ld = fi + 1;
+  const float AB = OR_A * OR_B;
+  for (int i = 0; i < fi; i++) {
+    float acc = 0.0f;
+    for (int j = 0; j < fo; j++) acc = acc + w[(int64_t)j * ld + i] * dd[j];
+    const float t = tanhf(OR_B * a_up[i]);
+    const float tt = t * t;
+    du[i] = (float)((double)acc * ((double)AB * (1.0 - (double)tt)));
+  }
+}
+
 float or_tanhf(float x) { return tanhf(x); }
 
 int or_set_threads(int n) {

@@ -74,6 +74,7 @@ def lib():
         L.or_fp_tiled.argtypes = [P, i32, i32, P, P, P]
         L.or_fp_naive.argtypes = [P, i32, i32, P, P, P]
         L.or_bp_tiled.argtypes = [P, i32, i32, P, P, P]
+        L.or_bp_naive.argtypes = [P, i32, i32, P, P, P]
         L.or_update.argtypes = [P, i32, i32, P, P, f32]
         L.or_tanhf.restype = f32
         L.or_tanhf.argtypes = [f32]
@@ -214,6 +215,16 @@ def backprop_tiled(w: np.ndarray, delta_down: np.ndarray, a_up: np.ndarray) -> n
     return du
 
 
+def backprop_naive(w: np.ndarray, delta_down: np.ndarray, a_up: np.ndarray) -> np.ndarray:
+    """kernels.py:74-83 (the reference's naive variant)."""
+    fo, ld = w.shape
+    du = np.empty(ld - 1, dtype=np.float32)
+    dd = np.ascontiguousarray(delta_down, dtype=np.float32)
+    au = np.ascontiguousarray(a_up, dtype=np.float32)
+    lib().or_bp_naive(_p(w), fo, ld - 1, _p(dd), _p(au), _p(du))
+    return du
+
+
 def update(w: np.ndarray, delta: np.ndarray, y_in: np.ndarray, eta: float) -> None:
     """kernels.py:299-310 (in place)."""
     fo, ld = w.shape
@@ -222,37 +233,46 @@ def update(w: np.ndarray, delta: np.ndarray, y_in: np.ndarray, eta: float) -> No
     lib().or_update(_p(w), fo, ld - 1, _p(d), _p(y), float(np.float32(eta)))
 
 
-def train_step(layers: list, x, digit: int, eta: float) -> np.ndarray:
-    """kernels.py:329-361 (tiled): FP all layers, output delta, BP, updates.
+def train_step(layers: list, x, digit: int, eta: float, variant: str = "tiled") -> np.ndarray:
+    """kernels.py:329-361: FP all layers, output delta, BP, updates.  variant
+    "tiled" (the one trainer.train uses) or "naive" (kernels.py:58-94; its
+    arithmetic differs from "tiled" only in the summation orders).
 
     Mutates `layers` (list of C-contiguous float32 (fo, fi+1)) in place and
     returns the output activations."""
+    fwd, bwd = (forward_tiled, backprop_tiled) if variant == "tiled" else (forward_naive,
+                                                                          backprop_naive)
     x0 = np.ascontiguousarray(np.asarray(x, dtype=np.float32).ravel())
     pre, out = [], []
     h = x0
     for w in layers:
-        a, y = forward_tiled(w, h)
+        a, y = fwd(w, h)
         pre.append(a)
         out.append(y)
         h = y
     deltas = [None] * len(layers)
     deltas[-1] = output_deltas(out[-1], pre[-1], digit)
     for li in range(len(layers) - 1, 0, -1):
-        deltas[li - 1] = backprop_tiled(layers[li], deltas[li], pre[li - 1])
+        deltas[li - 1] = bwd(layers[li], deltas[li], pre[li - 1])
     for li, w in enumerate(layers):
         update(w, deltas[li], x0 if li == 0 else out[li - 1], eta)
     return out[-1]
 
 
-def train_epoch(layers: list, images, labels, eta: float, order=None) -> int:
-    """trainer.py:104-123: returns the number of wrong argmax predictions."""
+def train_epoch(layers: list, images, labels, eta: float, order=None, preds=None,
+                variant: str = "tiled") -> int:
+    """trainer.py:104-123: returns the number of wrong argmax predictions;
+    `preds` (optional list) receives every sample's argmax in training order."""
     n = len(labels)
     flat = np.asarray(images, dtype=np.float32).reshape(n, -1)
     order = np.arange(n) if order is None else order
     wrong = 0
     for i in order:
-        y = train_step(layers, flat[i], int(labels[i]), eta)
-        if int(np.argmax(y)) != int(labels[i]):
+        y = train_step(layers, flat[i], int(labels[i]), eta, variant)
+        p = int(np.argmax(y))
+        if preds is not None:
+            preds.append(p)
+        if p != int(labels[i]):
             wrong += 1
     return wrong
 

@@ -47,7 +47,7 @@ SIGNATURES = [
     ("dmlp_net_set_layer", ctypes.c_int, [P, i32, P, i64]),
     ("dmlp_net_get_layer", ctypes.c_int, [P, i32, P, i64]),
     ("dmlp_train_step", ctypes.c_int, [P, P, i32, f32, P]),
-    ("dmlp_train_epoch", ctypes.c_int, [P, P, i64, P, P, i64, f32, P, P, P]),
+    ("dmlp_train_epoch", ctypes.c_int, [P, P, i64, P, P, i64, f32, P, P, P, P]),
     ("dmlp_forward_batch", ctypes.c_int, [P, P, i64, P, P]),
     ("dmlp_eval_counts", ctypes.c_int, [P, P, P, i64, P, P, P]),
     ("dmlp_deform", ctypes.c_int, [P, P, i64, i64, u64, u64, ctypes.POINTER(DeformParamsC), P, P]),

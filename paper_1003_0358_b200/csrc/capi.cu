@@ -51,6 +51,19 @@ int net_end(dmlp_net* net, cudaStream_t st) {
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// Plan-override knobs for A/B experiments (DMLP_YFLAT, DMLP_GS,
+// DMLP_FORCE_VARIANT, DMLP_FEAT).  Read only in builds made with
+// -DDMLP_EXPERIMENT_KNOBS (scripts/ab_perf.sh); the product library never
+// lets the environment change a net's kernel plan.
+static const char* knob(const char* name) {
+#ifdef DMLP_EXPERIMENT_KNOBS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 // Reference layout (fo, fi+1) row-major -> device rows of `pitch` floats.
 __global__ void k_pack(const float* __restrict__ src, float* __restrict__ dst, int fo, int fi,
                        int pitch) {
@@ -180,10 +193,10 @@ static void set_geometry(dmlp_net* net, int nct, size_t* yoff, size_t* poff, int
     // flat y words: a consumer's quad is then always one 32-byte pair of
     // vector polls (per-producer slots only give that when R % 4 == 0)
     ly.yflat = (ly.R & 3) != 0;
-    if (const char* yf = getenv("DMLP_YFLAT")) ly.yflat = atoi(yf) == 2 ? 1 : atoi(yf) == 0 ? 0 : ly.yflat;
+    if (const char* yf = knob("DMLP_YFLAT")) ly.yflat = atoi(yf) == 2 ? 1 : atoi(yf) == 0 ? 0 : ly.yflat;
     ly.pstride = round_up(ly.fi, 16);
     int force_gs = -1;  // experiments: DMLP_GS="gs0,gs1,..." per hidden layer, -1 = auto
-    if (const char* g = getenv("DMLP_GS")) {
+    if (const char* g = knob("DMLP_GS")) {
       for (int i = 0; i < l && g; i++) g = strchr(g, ',') ? strchr(g, ',') + 1 : nullptr;
       if (g) force_gs = atoi(g);
     }
@@ -229,7 +242,7 @@ static double auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
   for (int vi = 0; vi < nv; vi++) {
     const TrainVariant& tv = vars[vi];
     if (noreg && tv.n_reg > 0) continue;
-    if (const char* fv = getenv("DMLP_FORCE_VARIANT"))  // experiments: only plan `fv`
+    if (const char* fv = knob("DMLP_FORCE_VARIANT"))  // experiments: only plan `fv`
       if (atoi(fv) != vi) continue;
     unsigned regmask = 0;
     long long regf = 0;
@@ -308,10 +321,12 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
   if (sizes[n_sizes - 1] > kMaxOut)
     return set_error(DMLP_EINVAL, "output layer wider than %d is not supported", kMaxOut);
   const bool noreg = (residency & DMLP_RES_NOREG) != 0;
-  residency &= ~DMLP_RES_NOREG;
+  const bool allpaths = (residency & DMLP_RES_ALLPATHS) != 0;
+  residency &= ~(DMLP_RES_NOREG | DMLP_RES_ALLPATHS);
   if ((residency < DMLP_RES_AUTO || residency > DMLP_RES_SMEM) && !(residency & DMLP_RES_MASK))
     return set_error(DMLP_EINVAL, "unknown residency %d", residency);
-  DMLP_CUDA(cudaSetDevice(device));
+  DeviceGuard dg(device);
+  DMLP_CUDA(dg.err);
   cudaDeviceProp prop;
   DMLP_CUDA(cudaGetDeviceProperties(&prop, device));
   if (prop.major < 10)
@@ -419,7 +434,7 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     int feat = 0;
     for (int l = 0; l < H; l++)
       feat |= d.ly[l].res == kResSmem ? kFeatSmem : d.ly[l].res == kResL2 ? kFeatL2 : 0;
-    if (const char* f = getenv("DMLP_FEAT")) feat |= atoi(f);  // debugging aid: more paths
+    if (allpaths) feat = kFeatSmem | kFeatL2;  // sanitizer runs: every residency path
     net->train_fn = train_instance(vars[net->variant], feat);
     net->train_fn_prof = vars[net->variant].fn_prof;
   }
@@ -477,7 +492,7 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
 
 int dmlp_net_destroy(dmlp_net* net) {
   if (!net) return DMLP_OK;
-  cudaSetDevice(net->device);
+  DeviceGuard dg(net->device);
   cudaDeviceSynchronize();
   cudaFree(net->d_w);
   cudaFree(net->d_ll);
@@ -514,7 +529,8 @@ int dmlp_net_layer_residency(dmlp_net* net, int32_t* where) {
 
 int dmlp_net_profile(dmlp_net* net, int32_t enable) {
   if (!net) return set_error(DMLP_EINVAL, "null net");
-  DMLP_CUDA(cudaSetDevice(net->device));
+  DeviceGuard dg(net->device);
+  DMLP_CUDA(dg.err);
   DMLP_CUDA(cudaStreamSynchronize(net->stream));
   if (enable && !net->dev.prof) {
     unsigned long long* p = nullptr;
@@ -524,7 +540,6 @@ int dmlp_net_profile(dmlp_net* net, int32_t enable) {
   } else if (!enable && net->dev.prof) {
     DMLP_CUDA(cudaDeviceSynchronize());
     cudaFree(net->dev.prof);
-  cudaFree(net->dev.trace);
     net->dev.prof = nullptr;
   }
   return DMLP_OK;
@@ -532,7 +547,8 @@ int dmlp_net_profile(dmlp_net* net, int32_t enable) {
 
 int dmlp_net_trace(dmlp_net* net, int64_t sample, uint64_t* marks /* [n_ctas][64] or NULL */) {
   if (!net) return set_error(DMLP_EINVAL, "null net");
-  DMLP_CUDA(cudaSetDevice(net->device));
+  DeviceGuard dg(net->device);
+  DMLP_CUDA(dg.err);
   DMLP_CUDA(cudaDeviceSynchronize());
   const size_t bytes = (size_t)net->dev.nct * 64 * sizeof(unsigned long long);
   if (marks && net->dev.trace) {  // read back the previous launch's marks
@@ -552,7 +568,8 @@ int dmlp_net_trace(dmlp_net* net, int64_t sample, uint64_t* marks /* [n_ctas][64
 int dmlp_net_read_profile_all(dmlp_net* net, int64_t* slots, int32_t n_slots) {
   if (!net || !slots) return set_error(DMLP_EINVAL, "null argument");
   if (!net->dev.prof) return set_error(DMLP_EINVAL, "profiling is not enabled");
-  DMLP_CUDA(cudaSetDevice(net->device));
+  DeviceGuard dg(net->device);
+  DMLP_CUDA(dg.err);
   DMLP_CUDA(cudaDeviceSynchronize());
   const int n = kProfWords * net->dev.nct;
   unsigned long long* h = new unsigned long long[n];
@@ -584,7 +601,8 @@ int dmlp_net_set_layer(dmlp_net* net, int32_t layer, const float* w, int64_t n) 
   if (n != (int64_t)h.fo * (h.fi + 1))
     return set_error(DMLP_ESIZE, "layer %d holds %lld weights, got %lld", layer,
                      (long long)h.fo * (h.fi + 1), (long long)n);
-  DMLP_CUDA(cudaSetDevice(net->device));
+  DeviceGuard dg(net->device);
+  DMLP_CUDA(dg.err);
   float* tmp = nullptr;
   DMLP_CUDA(cudaStreamWaitEvent(net->stream, net->done, 0));
   DMLP_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), net->stream));
@@ -604,7 +622,8 @@ int dmlp_net_get_layer(dmlp_net* net, int32_t layer, float* w, int64_t n) {
   if (n != (int64_t)h.fo * (h.fi + 1))
     return set_error(DMLP_ESIZE, "layer %d holds %lld weights, got %lld", layer,
                      (long long)h.fo * (h.fi + 1), (long long)n);
-  DMLP_CUDA(cudaSetDevice(net->device));
+  DeviceGuard dg(net->device);
+  DMLP_CUDA(dg.err);
   float* tmp = nullptr;
   DMLP_CUDA(cudaStreamWaitEvent(net->stream, net->done, 0));
   DMLP_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), net->stream));
@@ -629,7 +648,7 @@ static int check_kernel_error(dmlp_net* net, cudaError_t e) {
 
 static int run_epoch(dmlp_net* net, const float* x, long long ldx, const uint8_t* labels,
                      const int32_t* order, long long n, float eta, long long* wrong, float* y_last,
-                     cudaStream_t st) {
+                     uint8_t* pred, cudaStream_t st) {
   if (n <= 0) return DMLP_OK;
   if (n > 0x7FFFFFFFLL) return set_error(DMLP_EINVAL, "at most 2^31-1 samples per launch");
   if (!(eta >= 0.0f)) return set_error(DMLP_EINVAL, "eta must be non-negative");
@@ -644,7 +663,7 @@ static int run_epoch(dmlp_net* net, const float* x, long long ldx, const uint8_t
   }
   const uint32_t seq0 = net->seq;
   if (int rc = net_begin(net, st)) return rc;
-  cudaError_t e = launch_train(net, x, ldx, labels, order, n, eta, seq0, wrong, y_last, st);
+  cudaError_t e = launch_train(net, x, ldx, labels, order, n, eta, seq0, wrong, y_last, pred, st);
   if (e != cudaSuccess) return check_kernel_error(net, e);
   if (int rc = net_end(net, st)) return rc;
   net->seq += (uint32_t)n;
@@ -655,7 +674,8 @@ int dmlp_train_step(dmlp_net* net, const float* x, int32_t digit, float eta, flo
   if (!net || !x) return set_error(DMLP_EINVAL, "null argument");
   const int nout = net->sizes[net->n_sizes - 1];
   if (digit < 0 || digit >= nout) return set_error(DMLP_EINVAL, "digit %d out of range", digit);
-  DMLP_CUDA(cudaSetDevice(net->device));
+  DeviceGuard dg(net->device);
+  DMLP_CUDA(dg.err);
   const int fi0 = net->sizes[0];
   uint8_t lab = (uint8_t)digit;
   DMLP_CUDA(cudaStreamWaitEvent(net->stream, net->done, 0));
@@ -663,7 +683,7 @@ int dmlp_train_step(dmlp_net* net, const float* x, int32_t digit, float eta, flo
   DMLP_CUDA(cudaMemcpyAsync(net->d_stage_lab, &lab, 1, cudaMemcpyHostToDevice, net->stream));
   float* ydev = net->d_stage + round_up(fi0, 32);
   int rc = run_epoch(net, net->d_stage, fi0, net->d_stage_lab, nullptr, 1, eta, nullptr, ydev,
-                     net->stream);
+                     nullptr, net->stream);
   if (rc) return rc;
   if (y_out)
     DMLP_CUDA(cudaMemcpyAsync(y_out, ydev, nout * sizeof(float), cudaMemcpyDefault, net->stream));
@@ -672,12 +692,13 @@ int dmlp_train_step(dmlp_net* net, const float* x, int32_t digit, float eta, flo
 
 int dmlp_train_epoch(dmlp_net* net, const float* x_dev, int64_t ldx, const uint8_t* labels_dev,
                      const int32_t* order_dev, int64_t n, float eta, int64_t* wrong_dev,
-                     float* y_last_dev, void* stream) {
+                     float* y_last_dev, uint8_t* pred_dev, void* stream) {
   if (!net || (!x_dev && n > 0) || (!labels_dev && n > 0))
     return set_error(DMLP_EINVAL, "null argument");
-  DMLP_CUDA(cudaSetDevice(net->device));
+  DeviceGuard dg(net->device);
+  DMLP_CUDA(dg.err);
   return run_epoch(net, x_dev, ldx, labels_dev, order_dev, n, eta, (long long*)wrong_dev,
-                   y_last_dev, (cudaStream_t)stream);
+                   y_last_dev, pred_dev, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -107,13 +107,28 @@ struct dmlp_net {
 };
 
 namespace dmlp {
+// Makes `device` current for the scope of an entry point and restores the
+// caller's device on exit (torch's current device is never changed behind
+// its back).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != device) err = cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 int set_error(int code, const char* fmt, ...);
 int cuda_check(cudaError_t e, const char* what);
 int net_begin(dmlp_net* net, cudaStream_t st);
 int net_end(dmlp_net* net, cudaStream_t st);
 cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
                          const uint8_t* labels, const int32_t* order, long long n, float eta,
-                         uint32_t seq0, long long* wrong, float* y_last, cudaStream_t st);
+                         uint32_t seq0, long long* wrong, float* y_last, uint8_t* pred,
+                         cudaStream_t st);
 // Compiled instantiations of the training kernel: n_reg register row blocks
 // of at most rr rows x rc columns per thread (0 = none), plus rs column
 // slots per thread in shared memory.

@@ -179,7 +179,8 @@ static int ensure_act(dmlp_net* net, size_t rows, int ld) {
 static int run_eval(dmlp_net* net, const float* x, long long n, float* out, const uint8_t* labels,
                     long long* counts, int* guess, cudaStream_t st) {
   if (n <= 0) return DMLP_OK;
-  if (int rc = cuda_check(cudaSetDevice(net->device), "cudaSetDevice")) return rc;
+  DeviceGuard dg(net->device);
+  if (int rc = cuda_check(dg.err, "cudaSetDevice")) return rc;
   const int L = net->dev.L;
   int maxld = 4;  // activation row stride = input pitch of the consuming layer
   for (int l = 1; l < L; l++) maxld = maxld > net->hl[l].pitch ? maxld : net->hl[l].pitch;

@@ -55,10 +55,11 @@ cudaError_t train_occupancy(const void* fn, int smem_bytes, int* blocks_per_sm) 
 
 cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
                          const uint8_t* labels, const int32_t* order, long long n, float eta,
-                         uint32_t seq0, long long* wrong, float* y_last, cudaStream_t st) {
+                         uint32_t seq0, long long* wrong, float* y_last, uint8_t* pred,
+                         cudaStream_t st) {
   NetDev nd = net->dev;
   unsigned long long* w = reinterpret_cast<unsigned long long*>(wrong);
-  void* args[] = {&nd, &x, &ldx, &labels, &order, &n, &eta, &seq0, &w, &y_last};
+  void* args[] = {&nd, &x, &ldx, &labels, &order, &n, &eta, &seq0, &w, &y_last, &pred};
   const void* fn = (nd.prof || nd.trace) ? net->train_fn_prof : net->train_fn;
   return cudaLaunchCooperativeKernel(fn, dim3(nd.nct), dim3(kThreads), args,
                                      (size_t)net->smem_bytes, st);

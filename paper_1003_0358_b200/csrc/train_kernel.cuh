@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_train(const NetDev net, const float* __restrict__ X, long long ldx,
             const uint8_t* __restrict__ labels, const int32_t* __restrict__ order,
             long long n, float eta, uint32_t seq0, unsigned long long* wrong_out,
-            float* y_last) {
+            float* y_last, uint8_t* pred) {
   extern __shared__ __align__(16) float sm[];
   __shared__ int g_r0[kMaxLayers], g_nr[kMaxLayers];
   __shared__ int g_rb[kMaxLayers];  // forward reduction buffer offset per layer
@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (yk > bv || yk != yk) { bv = yk; best = k; }
         }
         s_wrong += (best != digit);
+        if (pred != nullptr) pred[s] = (uint8_t)best;
       }
     };
 

@@ -85,12 +85,13 @@ def deform_device(raw, labels, params: DeformParams, seed: int, epoch: int, firs
     if out is None:
         out = torch.empty((n, GRID * GRID), dtype=torch.float32, device=raw.device)
     pc = params.to_c()
-    _lib.check(_lib.lib().dmlp_deform(ctypes.c_void_p(raw.data_ptr()),
-                                      ctypes.c_void_p(labels.data_ptr()), int(first), n,
-                                      int(seed) & 0xFFFFFFFFFFFFFFFF,
-                                      int(epoch) & 0xFFFFFFFFFFFFFFFF, ctypes.byref(pc),
-                                      ctypes.c_void_p(out.data_ptr()),
-                                      _stream(raw.device.index)), "dmlp_deform")
+    with torch.cuda.device(raw.device):  # the kernel launches on the current device
+        _lib.check(_lib.lib().dmlp_deform(ctypes.c_void_p(raw.data_ptr()),
+                                          ctypes.c_void_p(labels.data_ptr()), int(first), n,
+                                          int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                          int(epoch) & 0xFFFFFFFFFFFFFFFF, ctypes.byref(pc),
+                                          ctypes.c_void_p(out.data_ptr()),
+                                          _stream(raw.device.index)), "dmlp_deform")
     return out
 
 
@@ -101,11 +102,12 @@ def deform_injected_device(raw, noise_dx, noise_dy, scalars, kernel_size: int = 
     n = int(raw.shape[0])
     if out is None:
         out = torch.empty((n, GRID * GRID), dtype=torch.float32, device=raw.device)
-    _lib.check(_lib.lib().dmlp_deform_injected(
-        ctypes.c_void_p(raw.data_ptr()), n, ctypes.c_void_p(noise_dx.data_ptr()),
-        ctypes.c_void_p(noise_dy.data_ptr()), ctypes.c_void_p(scalars.data_ptr()),
-        int(kernel_size), ctypes.c_void_p(out.data_ptr()), _stream(raw.device.index)),
-        "dmlp_deform_injected")
+    with torch.cuda.device(raw.device):
+        _lib.check(_lib.lib().dmlp_deform_injected(
+            ctypes.c_void_p(raw.data_ptr()), n, ctypes.c_void_p(noise_dx.data_ptr()),
+            ctypes.c_void_p(noise_dy.data_ptr()), ctypes.c_void_p(scalars.data_ptr()),
+            int(kernel_size), ctypes.c_void_p(out.data_ptr()), _stream(raw.device.index)),
+            "dmlp_deform_injected")
     return out
 
 
@@ -114,9 +116,10 @@ def upscale_device(raw, out=None):
     n = int(raw.shape[0])
     if out is None:
         out = torch.empty((n, GRID * GRID), dtype=torch.float32, device=raw.device)
-    _lib.check(_lib.lib().dmlp_upscale(ctypes.c_void_p(raw.data_ptr()), n,
-                                       ctypes.c_void_p(out.data_ptr()),
-                                       _stream(raw.device.index)), "dmlp_upscale")
+    with torch.cuda.device(raw.device):
+        _lib.check(_lib.lib().dmlp_upscale(ctypes.c_void_p(raw.data_ptr()), n,
+                                           ctypes.c_void_p(out.data_ptr()),
+                                           _stream(raw.device.index)), "dmlp_upscale")
     return out
 
 

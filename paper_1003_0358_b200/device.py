@@ -36,7 +36,8 @@ def current_stream_handle(device: int = 0) -> ctypes.c_void_p:
 class DeviceNet:
     """Padded, device-resident copy of an Mlp plus the persistent-kernel state."""
 
-    def __init__(self, layer_sizes, device: int = 0, residency: str = "auto", n_ctas: int = 0):
+    def __init__(self, layer_sizes, device: int = 0, residency: str = "auto", n_ctas: int = 0,
+                 all_paths: bool = False):
         _torch()
         self.layer_sizes = tuple(int(s) for s in layer_sizes)
         self.device = int(device)
@@ -46,6 +47,8 @@ class DeviceNet:
             code = 0x10000 | residency
         else:
             code = (_lib.RES_AUTO | 0x20000) if residency == "auto-noreg" else _lib.RESIDENCY[residency]
+        if all_paths:  # kernel instance with every residency path (sanitizer coverage)
+            code |= 0x40000
         _lib.check(_lib.lib().dmlp_net_create(self.device, sizes, len(self.layer_sizes), code,
                                               int(n_ctas), ctypes.byref(h)), "dmlp_net_create")
         self._h = h
@@ -89,6 +92,9 @@ class DeviceNet:
                 p = w.ctypes.data_as(ctypes.c_void_p)
             else:  # torch tensor (host or device)
                 w = w.contiguous().float()
+                if w.is_cuda:  # the copy/conversion (or a broadcast) runs on torch's
+                    # stream; dmlp_net_set_layer reads on the net's own stream
+                    _torch().cuda.current_stream(w.device).synchronize()
                 p = _ptr(w)
             _lib.check(_lib.lib().dmlp_net_set_layer(self._h, li, p, w.size if isinstance(
                 w, np.ndarray) else w.numel()), "dmlp_net_set_layer")
@@ -150,19 +156,52 @@ class DeviceNet:
                    "dmlp_train_step")
         return y
 
-    def train_epoch(self, x, labels, order, eta: float, wrong, y_last=None, stream=None) -> None:
+    def _check_cuda(self, name, t, dtype, dim=None):
+        torch = _torch()
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{name} must be a CUDA tensor on cuda:{self.device}")
+        if t.dtype != dtype:
+            raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+        if dim is not None and t.dim() != dim:
+            raise SizeMismatch(f"{name} must have {dim} dimensions, got shape {tuple(t.shape)}")
+
+    def train_epoch(self, x, labels, order, eta: float, wrong, y_last=None, stream=None,
+                    pred=None, check_order: bool = True) -> None:
         """Asynchronous on `stream` (default: torch's current stream).
 
-        x: (n, >=fan_in) f32 CUDA tensor; labels: (n,) u8; order: (n,) i32 or
-        None; wrong: int64 CUDA scalar accumulating argmax errors."""
+        x: (n, >=fan_in) f32 CUDA tensor, unit column stride; labels: (n,) u8;
+        order: (m,) i32 with values in [0, n), or None; wrong: int64 CUDA
+        scalar accumulating argmax errors; pred (optional): (m,) u8 receiving
+        every sample's argmax in training order."""
+        torch = _torch()
         if eta < 0:
             raise ValueError("eta must be non-negative")
+        self._check_cuda("x", x, torch.float32, 2)
+        self._check_cuda("labels", labels, torch.uint8, 1)
+        self._check_cuda("wrong", wrong, torch.int64)
+        if x.stride(1) != 1 or x.shape[1] < self.layer_sizes[0]:
+            raise SizeMismatch(f"x must be (n, >= {self.layer_sizes[0]}) with unit column stride")
+        if labels.numel() < x.shape[0] or not labels.is_contiguous():
+            raise SizeMismatch(f"{labels.numel()} labels for {x.shape[0]} rows")
+        if order is not None:
+            self._check_cuda("order", order, torch.int32, 1)
+            if not order.is_contiguous():
+                raise ValueError("order must be contiguous")
+            if check_order and order.numel() and (int(order.min()) < 0 or
+                                                  int(order.max()) >= x.shape[0]):
+                raise ValueError(f"order values must lie in [0, {x.shape[0]})")
         n = int(order.numel()) if order is not None else int(x.shape[0])
+        if pred is not None:
+            self._check_cuda("pred", pred, torch.uint8, 1)
+            if pred.numel() < n or not pred.is_contiguous():
+                raise SizeMismatch(f"pred holds {pred.numel()} entries for {n} samples")
+        if y_last is not None:
+            self._check_cuda("y_last", y_last, torch.float32)
         ldx = int(x.stride(0))
         st = stream if stream is not None else current_stream_handle(self.device)
         _lib.check(_lib.lib().dmlp_train_epoch(self._h, _ptr(x), ldx, _ptr(labels), _ptr(order),
                                                n, float(np.float32(eta)), _ptr(wrong),
-                                               _ptr(y_last), st), "dmlp_train_epoch")
+                                               _ptr(y_last), _ptr(pred), st), "dmlp_train_epoch")
 
     # -- evaluation ---------------------------------------------------------------
     def forward_batch(self, x, out=None, stream=None):
@@ -183,8 +222,19 @@ class DeviceNet:
         n = int(x.shape[0])
         if x.dim() != 2 or x.shape[1] != self.layer_sizes[0] or not x.is_contiguous():
             raise SizeMismatch(f"batch shape {tuple(x.shape)}, want (n, {self.layer_sizes[0]})")
+        self._check_cuda("x", x, torch.float32, 2)
+        self._check_cuda("labels", labels, torch.uint8, 1)
+        if labels.numel() != n or not labels.is_contiguous():
+            raise SizeMismatch(f"{labels.numel()} labels for {n} samples")
         if counts is None:
             counts = torch.zeros(102, dtype=torch.int64, device=x.device)
+        self._check_cuda("counts", counts, torch.int64, 1)
+        if counts.numel() != 102:
+            raise SizeMismatch("counts must hold 102 int64")
+        if guess is not None:
+            self._check_cuda("guess", guess, torch.int32, 2)
+            if tuple(guess.shape) != (n, 2) or not guess.is_contiguous():
+                raise SizeMismatch(f"guess must be ({n}, 2) int32")
         st = stream if stream is not None else current_stream_handle(self.device)
         _lib.check(_lib.lib().dmlp_eval_counts(self._h, _ptr(x), _ptr(labels), n, _ptr(counts),
                                                _ptr(guess), st), "dmlp_eval_counts")

@@ -1,5 +1,6 @@
 #!/bin/bash
 # A/B one build under two environment settings: ENV_A / ENV_B (e.g. "DMLP_YFLAT=0")
+# needs a library built with the plan-override knobs: DMLP_NVCC_FLAGS=-DDMLP_EXPERIMENT_KNOBS python -m paper_1003_0358_b200.build --force
 for round in 1 2; do
 for v in A B; do
   e=ENV_$v

@@ -1,5 +1,6 @@
 #!/bin/bash
 # A/B the per-layer row-group mapping (DMLP_GS, capi.cu choose_mapping) on one box.
+# needs a library built with the plan-override knobs: DMLP_NVCC_FLAGS=-DDMLP_EXPERIMENT_KNOBS python -m paper_1003_0358_b200.build --force
 # usage: CFG=C4 GS_LIST="auto 2 3" bash scripts/gs_ab.sh
 for round in 1 2; do
 for g in ${GS_LIST:-auto}; do

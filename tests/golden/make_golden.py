@@ -130,6 +130,30 @@ def gen_train():
     np.savez_compressed(os.path.join(OUT, "train.npz"), **res)
 
 
+def gen_naive():
+    """The reference's naive variant (kernels.py:58-94) on the train fixture's
+    inputs: the yardstick for how far two summation orders of the same
+    arithmetic drift apart (tests/test_gpu_parity_deep.py)."""
+    g = np.load(os.path.join(OUT, "train.npz"))
+    x, labels = g["deformed"].reshape(64, -1), g["labels"]
+    arch = network.Architecture((841, 70, 33, 10))
+    mlp = network.init_mlp(rng.substream(0, rng.STREAM_INIT), arch)
+    outs = []
+    for s in range(40):
+        i = s % 64
+        outs.append(kernels.train_step(mlp, x[i], int(labels[i]), 1e-3, variant="naive"))
+    res = {"small_outputs": np.array(outs),
+           "small_final": np.concatenate([w.ravel() for w in mlp.layers])}
+    arch = network.Architecture(CONFIGS["C1"])
+    mlp = network.init_mlp(rng.substream(0, rng.STREAM_INIT), arch)
+    outs = []
+    for s in range(25):
+        outs.append(kernels.train_step(mlp, x[s], int(labels[s]), 1e-3, variant="naive"))
+    res["c1_outputs"] = np.array(outs)
+    res["c1_sha1"] = np.array([sha1(w) for w in mlp.layers])
+    np.savez_compressed(os.path.join(OUT, "naive.npz"), **res)
+
+
 def gen_eval_and_known():
     images, labels = make_digits(300, seed=31337)
     ds = Dataset(images, labels, "test")
@@ -173,11 +197,12 @@ def gen_gradcheck():
                         worst=np.float64(worst))
 
 
+GENERATORS = {"rng": gen_rng, "deform": gen_deform, "train": gen_train, "naive": gen_naive,
+              "eval": gen_eval_and_known, "gradcheck": gen_gradcheck}
+
 if __name__ == "__main__":
-    gen_rng()
-    gen_deform()
-    gen_train()
-    gen_eval_and_known()
-    gen_gradcheck()
+    # python tests/golden/make_golden.py [name ...]   (default: every fixture)
+    for name in (sys.argv[1:] or list(GENERATORS)):
+        GENERATORS[name]()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -117,4 +117,7 @@ def test_eval_big_nets_vs_oracle(sizes):
     assert np.abs(out - ref).max() <= 1e-5 * np.abs(ref).max()
     srt = np.sort(ref, axis=1)
     ok = (srt[:, -1] - srt[:, -2]) >= 1e-5
+    # near ties (top-2 margin under the logit tolerance) are counted and
+    # bounded; argmax must agree on every other sample
+    assert int((~ok).sum()) <= len(ok) // 200, f"{int((~ok).sum())} near ties"
     assert np.array_equal(np.argmax(out, 1)[ok], np.argmax(ref, 1)[ok])

@@ -10,44 +10,63 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _oracle_train(images, labels, sizes, epochs, seed=0):
-    """trainer.train restated with the oracle: deform -> shuffled on-line pass
-    -> validation on the un-deformed train set (counts)."""
+def _oracle_train(deformed_epochs, images, labels, sizes, seed=0):
+    """trainer.train restated with the oracle (trainer.py:130-207): shuffled
+    on-line pass over each epoch's deformed set -> validation on the
+    un-deformed train set (counts); weights snapshotted after every epoch."""
     layers = O.init_layers(seed, sizes)
     x_val = O.upscale_dataset(images)
-    hist = []
-    for e in range(epochs):
-        deformed = O.deform_epoch(images, labels, O.DeformParams(), seed=seed, epoch=e)
+    hist, snaps = [], []
+    for e, deformed in enumerate(deformed_epochs):
         eta = max(1e-6, 1e-3 * 0.993 ** e)
         perm = O.substream(seed, 3, e).permutation(len(labels))
         wrong = O.train_epoch(layers, deformed, labels, eta, order=perm)
         vwrong = O.eval_counts(O.forward_batch(layers, x_val), labels)[0]
         hist.append((wrong, vwrong))
-    return layers, hist
+        snaps.append([w.copy() for w in layers])
+    return hist, snaps
 
 
 def test_train_two_epochs_matches_oracle(tmp_path):
+    """trainer.train (C1, 3,000 images, 2 epochs) vs the oracle replay of the
+    reference protocol on the same deformed inputs: train and validation
+    error counts exact, the best epoch's weights within 1e-5 relative per
+    layer.  The deformed inputs are the device kernel's (a pure function of
+    seed, epoch and image; checked against the oracle's deformation within
+    1e-5 here, and bit-pinned in test_gpu_deform_eval)."""
+    import torch
+
+    from paper_1003_0358_b200.deform import DeformParams, deform_device
     from paper_1003_0358_b200.mnist_io import Dataset
     from paper_1003_0358_b200.network import Architecture, load_checkpoint
     from paper_1003_0358_b200.synthetic import make_digits
     from paper_1003_0358_b200.trainer import TrainConfig, train
 
-    imgs, labs = make_digits(600, seed=21)
-    sizes = (841, 120, 60, 10)
-    O.set_threads(8)
-    ref_layers, ref_hist = _oracle_train(imgs, labs, sizes, 2)
+    imgs, labs = make_digits(3000, seed=21)
+    sizes = (841, 1000, 500, 10)
+    O.set_threads(16)
+    raw, lab = torch.from_numpy(imgs).cuda(), torch.from_numpy(labs).cuda()
+    epochs = []
+    for e in range(2):
+        d = deform_device(raw, lab, DeformParams(), 0, e).cpu().numpy()
+        od = O.deform_epoch(imgs[:256], labs[:256], O.DeformParams(), seed=0, epoch=e)
+        assert np.abs(d[:256].reshape(-1, 29, 29) - od).max() <= 1e-5
+        epochs.append(d)
+    ref_hist, snaps = _oracle_train(epochs, imgs, labs, sizes)
     res = train(TrainConfig(arch=Architecture(sizes), max_epochs=2), Dataset(imgs, labs, "train"),
                 out_dir=tmp_path)
     n = len(labs)
     for (w, vw), st in zip(ref_hist, res.history):
-        assert abs(st.train_error - 100.0 * w / n) <= 100.0 / n + 1e-9
-        assert abs(st.val_error - 100.0 * vw / n) <= 100.0 / n + 1e-9
-    # weights of the last epoch (best_mlp may be earlier): compare the final net
-    # through the checkpoint of the best epoch when it is the last one
-    if res.best_epoch == 1:
-        ck = load_checkpoint((tmp_path / "best.dmlp").read_bytes())
-        for g, r in zip(ck.mlp.layers, ref_layers):
-            assert np.abs(g - r).max() <= 1e-5 * np.abs(r).max()
+        assert st.train_error == 100.0 * w / n, (st.epoch, st.train_error, 100.0 * w / n)
+        assert st.val_error == 100.0 * vw / n, (st.epoch, st.val_error, 100.0 * vw / n)
+    assert res.best_epoch in (0, 1)
+    ck = load_checkpoint((tmp_path / "best.dmlp").read_bytes())
+    assert ck.epoch == res.best_epoch
+    for li, (g, b, r) in enumerate(zip(ck.mlp.layers, res.best_mlp.layers,
+                                       snaps[res.best_epoch])):
+        assert np.array_equal(g, b)
+        rel = np.abs(g.astype(np.float64) - r).max() / np.abs(r).max()
+        assert rel <= 1e-5, f"layer {li}: max|dW|/max|W| = {rel:.2e}"
     assert (tmp_path / "run_history.jsonl").read_text().count("\n") == 2
 
 
@@ -147,3 +166,36 @@ def test_train_resume_replays_the_uninterrupted_run(tmp_path):
     if full.best_epoch == 1 and rest.best_epoch == 1:
         for a, b in zip(full.best_mlp.layers, rest.best_mlp.layers):
             assert np.array_equal(a, b)
+
+
+def test_resume_from_interrupt_checkpoint(tmp_path, monkeypatch):
+    """KeyboardInterrupt -> interrupt.dmlp stores the epoch that was running
+    (trainer.py:203-205); resuming from it continues at that epoch and
+    replays the uninterrupted run."""
+    from paper_1003_0358_b200 import trainer as T
+    from paper_1003_0358_b200.mnist_io import Dataset
+    from paper_1003_0358_b200.network import Architecture, load_checkpoint
+    from paper_1003_0358_b200.synthetic import make_digits
+
+    imgs, labs = make_digits(400, seed=6)
+    sizes = (841, 90, 40, 10)
+    ds = Dataset(imgs, labs, "train")
+    cfg = T.TrainConfig(arch=Architecture(sizes), max_epochs=3)
+    full = T.train(cfg, ds)
+    real = T.lr_schedule
+
+    def stop_at_epoch_1(epoch, c):
+        if epoch == 1:
+            raise KeyboardInterrupt
+        return real(epoch, c)
+
+    monkeypatch.setattr(T, "lr_schedule", stop_at_epoch_1)
+    with pytest.raises(T.InterruptCheckpoint) as ei:
+        T.train(cfg, ds, out_dir=tmp_path)
+    monkeypatch.setattr(T, "lr_schedule", real)
+    ck = load_checkpoint(ei.value.path.read_bytes())
+    assert ck.epoch == 1 and np.isnan(ck.validation_error)
+    rest = T.train(cfg, ds, resume=ei.value.path)
+    assert [h.epoch for h in rest.history] == [1, 2]
+    for a, b in zip(rest.history, full.history[1:]):
+        assert (a.train_error, a.val_error) == (b.train_error, b.val_error)

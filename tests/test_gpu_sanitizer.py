@@ -6,7 +6,7 @@ synccheck catches a barrier reached by a divergent warp -- the failure that
 made the register-only instance compute wrong weights -- and racecheck the
 shared-memory hazards between the phases.  Each check runs a few samples of
 a small net in a subprocess, once per compiled feature instance (register
-rows only; smem + L2 paths forced in with DMLP_FEAT).
+rows only; smem + L2 paths forced in with DMLP_RES_ALLPATHS).
 """
 
 import os
@@ -28,7 +28,7 @@ from paper_1003_0358_b200.device import DeviceNet
 g = np.load(%r); x = g['deformed'].reshape(64, -1); lab = g['labels']
 sizes = tuple(int(v) for v in sys.argv[1].split(','))
 n = int(sys.argv[2])
-dn = DeviceNet(sizes); dn.set_layers(O.init_layers(7, sizes))
+dn = DeviceNet(sizes, all_paths=sys.argv[3] == '3'); dn.set_layers(O.init_layers(7, sizes))
 wrong = torch.zeros((), dtype=torch.int64, device='cuda')
 dn.train_epoch(torch.from_numpy(x[:n]).cuda(), torch.from_numpy(lab[:n]).cuda(), None, 1e-3, wrong)
 torch.cuda.synchronize()
@@ -49,10 +49,9 @@ def _sanitizer():
 def test_train_kernel_sanitizer(tmp_path, tool, feat, sizes):
     script = tmp_path / "case.py"
     script.write_text(CASE)
-    env = dict(os.environ, DMLP_FEAT=feat)
     p = subprocess.run([_sanitizer(), "--tool", tool, "--print-limit", "4", "--error-exitcode", "9",
-                        sys.executable, str(script), sizes, "3"],
-                       env=env, capture_output=True, text=True, timeout=600)
+                        sys.executable, str(script), sizes, "3", feat],
+                       capture_output=True, text=True, timeout=600)
     out = p.stdout + p.stderr
     assert p.returncode == 0 and "ok " in out, out[-3000:]
     assert "ERROR SUMMARY: 0 errors" in out or "0 hazards" in out, out[-3000:]

@@ -182,33 +182,6 @@ def test_device_tanhf_matches_libm():
     assert same.all(), x[~same][:5]
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
-def test_train_epoch_headline_configs(golden, cfg):
-    """The BASELINE configs with their auto plans (CTA count, register row
-    blocks, shared memory and streamed layers): 160 on-line samples in one
-    launch vs the oracle's epoch on identical inputs."""
-    import torch
-
-    sizes = {"C1": (841, 1000, 500, 10), "C2": (841, 1500, 1000, 500, 10),
-             "C3": (841, 2000, 1500, 1000, 500, 10),
-             "C4": (841, 2500, 2000, 1500, 1000, 500, 10),
-             "C5": (841,) + (1000,) * 9 + (10,)}[cfg]
-    g = golden("train")
-    x, lab = _inputs(golden)
-    n = 160
-    order = (np.arange(n) * 37) % 64
-    ref = O.init_layers(0, sizes)
-    dn = _net(sizes, [w.copy() for w in ref])
-    O.set_threads(8)
-    wrong_ref = O.train_epoch(ref, g["deformed"], lab, 1e-3, order=order)
-    wrong = torch.zeros((), dtype=torch.int64, device="cuda")
-    dn.train_epoch(torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda(),
-                   torch.from_numpy(order.astype(np.int32)).cuda(), 1e-3, wrong)
-    torch.cuda.synchronize()
-    assert int(wrong.item()) == wrong_ref
-    _assert_weights_close(dn.get_layers(), ref)
-
-
 @pytest.mark.parametrize("sizes,n_ctas", [
     ((841, 10), 0),                      # no hidden layer: one CTA, output tile = all inputs
     ((841, 5000, 10), 0),                # 34 rows per CTA: two reduction chunks, > 32-row gathers
