@@ -137,9 +137,25 @@ def make_inputs(n_raw: int, seed: int, device: str):
 # ----------------------------------------------------------------------------- CPU legs
 
 
-def cpu_train_rate(sizes, seconds: float = 12.0, threads: int | None = None) -> dict:
-    """The reference algorithm (oracle port, bit-exact with kernels.train_step
-    tiled) on the host cores: on-line samples/s over a bounded sample."""
+def cpu_model() -> dict:
+    """The host CPU the CPU legs ran on (model name from /proc/cpuinfo, nproc)."""
+    name = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    name = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": name, "nproc": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None}
+
+
+def cpu_train_rate(sizes, seconds: float = 12.0, threads: int | None = None,
+                   variant: str = "tiled") -> dict:
+    """The reference algorithm (oracle port of kernels.train_step, `variant`
+    arithmetic) on the host cores: on-line samples/s over a bounded sample."""
     import numpy as np
 
     from oracle import oracle as O
@@ -151,28 +167,68 @@ def cpu_train_rate(sizes, seconds: float = 12.0, threads: int | None = None) -> 
     x = O.deform_epoch(imgs, labs, O.DeformParams(), seed=0, epoch=0).reshape(64, -1)
     layers = O.init_layers(0, sizes)
     for i in range(3):  # warm-up
-        O.train_step(layers, x[i], int(labs[i]), 1e-3)
+        O.train_step(layers, x[i], int(labs[i]), 1e-3, variant)
     n, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < seconds or n < 5:
-        O.train_step(layers, x[n % 64], int(labs[n % 64]), 1e-3)
+        O.train_step(layers, x[n % 64], int(labs[n % 64]), 1e-3, variant)
         n += 1
     dt = time.perf_counter() - t0
+    O.set_threads(os.cpu_count() or 1)
     return {"value": n / dt, "unit": "samples/s", "cores": threads, "kind": "port",
             "sample": f"{n} on-line train_step calls of {sizes} in {dt:.1f}s "
-                      f"(oracle/dmlp_oracle.c, tiled arithmetic, {threads} threads)"}
+                      f"(oracle/dmlp_oracle.c, {variant} arithmetic, {threads} threads)"}
 
 
-def cpu_deform_rate(seconds: float = 4.0, threads: int | None = None) -> dict:
+def cpu_deform_rate(seconds: float = 3.0, threads: int = 1) -> dict:
+    """deform_epoch (deform.py:217-247) at lanes=`threads` on a bounded sample."""
     from oracle import oracle as O
     from paper_1003_0358_b200.synthetic import make_digits
 
-    threads = threads or os.cpu_count() or 1
-    imgs, labs = make_digits(2048, seed=3)
+    imgs, labs = make_digits(512, seed=3)
     n, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < seconds or n == 0:
         O.deform_epoch(imgs, labs, O.DeformParams(), seed=0, epoch=n, threads=threads)
         n += len(imgs)
-    return {"value": n / (time.perf_counter() - t0), "unit": "imgs/s", "cores": threads}
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "imgs/s", "cores": threads, "kind": "port",
+            "sample": f"{n} images deformed in {dt:.1f}s (oracle/dmlp_oracle.c, lanes={threads})"}
+
+
+def cpu_forward_batch_rate(sizes, n_images: int = 10000) -> dict:
+    """network.forward_batch (network.py:118-130: OpenBLAS sgemm + numpy tanh)
+    on n_images un-deformed inputs, all host threads."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    layers = O.init_layers(0, sizes)
+    x = np.random.default_rng(5).uniform(-1, 1, size=(n_images, sizes[0])).astype(np.float32)
+    O.forward_batch(layers, x[:256])  # warm-up (BLAS thread pool)
+    t0 = time.perf_counter()
+    O.forward_batch(layers, x)
+    dt = time.perf_counter() - t0
+    flops = 2 * sum(i * o for i, o in zip(sizes[:-1], sizes[1:])) * n_images
+    return {"value": n_images / dt, "unit": "imgs/s", "cores": os.cpu_count(), "kind": "port",
+            "TFLOPs": round(flops / dt / 1e12, 3),
+            "sample": f"forward_batch of {n_images} images in {dt:.2f}s (numpy/OpenBLAS sgemm)"}
+
+
+def cpu_baseline_block(sizes, seconds: float) -> dict:
+    """cpu_baseline of the bench line: the headline leg (train_step tiled,
+    every host thread) plus the context legs BASELINE.md §2 asks for."""
+    cpu = cpu_train_rate(sizes, seconds=seconds)
+    short = max(1.0, seconds / 4)
+    cpu["cpu"] = cpu_model()
+    cpu["legs"] = {
+        "train_step_tiled_1thread": cpu_train_rate(sizes, seconds=short, threads=1),
+        "train_step_naive_all_threads": cpu_train_rate(sizes, seconds=short, variant="naive"),
+        "forward_batch_10k": cpu_forward_batch_rate(sizes),
+        "deform_epoch_lanes1": cpu_deform_rate(seconds=short, threads=1),
+    }
+    for leg in cpu["legs"].values():
+        leg["value"] = round(leg["value"], 2)
+    cpu["value"] = round(cpu["value"], 2)
+    return cpu
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -281,21 +337,24 @@ def run_gpu(args) -> dict | None:
         t = torch.tensor([dms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dms = float(t.item())
-    deform = {"imgs_per_s": nd / (dms / 1e3), "images": nd, "ms_per_epoch": round(dms, 3),
+    deform = {"imgs_per_s": nd / (dms / 1e3), "imgs_per_s_per_gpu": nd / (dms / 1e3) / world,
+              "images": nd, "n_gpus": world, "sharding": "image index ranges, no collective",
+              "ms_per_epoch": round(dms, 3),
               "bytes_per_img": 4149, "GBs": round(4149 * nd / (dms / 1e3) / 1e9, 1)}
 
-    # ---- evaluation: validation pass over the un-deformed training images
+    # ---- evaluation: validation pass over the un-deformed training images,
+    # sharded by rank + one all-reduce of the counts (eval_counts_sharded)
+    from paper_1003_0358_b200.distributed import broadcast_layers, eval_counts_sharded
+
     ev = DeviceNet(sizes, device=local)
     ev.set_layers(mlp.layers)
-    xv = upscale_device(d_imgs[lo:hi])
-    counts = torch.zeros(102, dtype=torch.int64, device=device)
-    ev.eval_counts(xv, d_lab[lo:hi], counts)
+    broadcast_layers(ev, src=0)  # every rank evaluates rank 0's weights
+    xv = upscale_device(d_imgs)
+    eval_counts_sharded(ev, xv, d_lab)
     barrier()
     a.record(stream)
-    ev.eval_counts(xv, d_lab[lo:hi], counts)
+    counts = eval_counts_sharded(ev, xv, d_lab)
     b.record(stream)
-    if world > 1:
-        dist.all_reduce(counts)  # the single NCCL all-reduce of the count vector
     barrier()
     ems = a.elapsed_time(b)
     if world > 1:
@@ -303,7 +362,9 @@ def run_gpu(args) -> dict | None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems = float(t.item())
     flops = 2 * sum(i * o for i, o in zip(sizes[:-1], sizes[1:]))
-    evaluation = {"imgs_per_s": nd / (ems / 1e3), "images": nd,
+    evaluation = {"imgs_per_s": nd / (ems / 1e3), "imgs_per_s_per_gpu": nd / (ems / 1e3) / world,
+                  "images": nd, "n_gpus": world, "wrong": int(counts[0].item()),
+                  "sharding": "samples by rank + one NCCL all_reduce of int64[102] (timed)",
                   "TFLOPs": round(flops * nd / (ems / 1e3) / 1e12, 2)}
 
     if rank != 0:
@@ -315,19 +376,41 @@ def run_gpu(args) -> dict | None:
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = 12.0 * W * sps_rank / 1e9
     l2 = l2_peak()
+    smem_peak = smem_peak_gbs(clk.summary().get("sm_mhz"))
+    levels = level_bytes(sizes, dn)
+    t_min = (levels["smem"] / (smem_peak * 1e9) + levels["l2"] / (l2 * 1e9)) if l2 else None
     traffic = profiled_traffic(args.config, n)
     roofline = {
-        "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-        "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+        # the weights live in registers / shared memory / L2 (layer_residency),
+        # never in HBM inside the loop: the bound is the L2 read+write peak
+        # (BASELINE.md §3), measured live in this run (K6)
+        "bound": "l2", "achieved": round(achieved, 1), "peak": l2, "unit": "GB/s",
+        "frac": round(achieved / l2, 4) if l2 else None,
+        "peak_source": "K6 L2-resident read+write copy (48 MB, one CTA per SM), measured in "
+                       "this run (paper_1003_0358_b200/csrc/microbench.cu)",
+        "traffic": traffic,
+        "traffic_source": (f"DRAM bytes per sample from the committed ncu --set full capture "
+                           f"profiles/ncu_train_{args.config.lower()}.json, scaled to {n} "
+                           "samples (not measured in this run)") if traffic else None,
         "algorithmic_bytes_per_sample": 12 * W,
         "algorithmic_bytes_per_launch": 12 * W * n,
         "residency": dn.residency,
-        "l2_peak_rw_GBs": l2, "frac_of_l2_rw": round(achieved / l2, 4) if l2 else None,
+        # SURVEY.md §8(d) hybrid roofline: t_min = sum over levels of the 12 B
+        # per weight each level serves / that level's peak (registers free)
+        "hybrid": {
+            "bytes_per_sample": levels,
+            "smem_peak_GBs": round(smem_peak, 1), "l2_peak_GBs": l2,
+            "t_min_us": round(t_min * 1e6, 3) if t_min else None,
+            "t_measured_us": round(1e6 / sps_rank, 3),
+            "frac_hybrid": round(t_min * sps_rank, 4) if t_min else None,
+        },
+        "hbm_peak_GBs": hbm_peak, "frac_of_hbm": round(achieved / hbm_peak, 4),
+        "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+        "target_samples_per_s_at_0.70_of_l2": round(0.7 * l2 * 1e9 / (12 * W), 1) if l2 else None,
         "exchange_fraction": round(prof["exchange_fraction"], 3),
         "sync_bound": sync_bound(len(sizes) - 1, sps_rank),
     }
-    cpu = cpu_train_rate(sizes, seconds=args.cpu_seconds) if args.cpu_seconds > 0 else None
+    cpu = cpu_baseline_block(sizes, args.cpu_seconds) if args.cpu_seconds > 0 else None
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -366,6 +449,43 @@ def bench_config(args, world: int) -> dict:
                    f"inputs SMALLER than L2 ({n * 841 * 4 / 1e6:.0f} MB per step), ")
                   + "each input row read once per step; weights are deliberately kept on chip "
                     "(smem / registers) or in L2"}
+
+
+def smem_peak_gbs(sm_mhz) -> float:
+    """Shared-memory bandwidth of the whole chip: 148 SMs x 128 B/clk at the
+    SM clock sampled during the timed region (max clock if none)."""
+    mhz = float(sm_mhz or measured_peaks().get("sm_max_mhz", 1965.0))
+    return 148 * 128 * mhz * 1e6 / 1e9
+
+
+def level_bytes(sizes, dn) -> dict:
+    """Algorithmic bytes per sample (12 per weight) by the level that serves
+    them in the training kernel: registers, shared memory, L2."""
+    out = {"reg": 0, "smem": 0, "l2": 0}
+    for li, (fi, fo) in enumerate(zip(sizes[:-1], sizes[1:])):
+        fi1 = fi + 1
+        where = dn.layer_residency[li] if li < len(sizes) - 2 else "smem"  # output tile: smem
+        if where == "reg":
+            rc = dn.layer_reg_cols[li]
+            out["reg"] += 12 * fo * rc
+            out["smem"] += 12 * fo * (fi1 - rc)  # the plan's shared-memory tail
+        else:
+            out[where] += 12 * fo * fi1
+    return out
+
+
+def relaunch_under_torchrun(n: int) -> None:
+    """`python bench.py --gpus N` without torchrun: re-exec as N ranks (one
+    process per GPU, 127.0.0.1 rendezvous), the same launch the driver uses."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 def l2_peak() -> float | None:
@@ -459,6 +579,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
+    if args.gpus > 1 and dist_env()[1] != args.gpus:
+        sys.exit(f"--gpus {args.gpus} but WORLD_SIZE={dist_env()[1]}")
     line = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if line is not None:
         print(json.dumps(line), flush=True)

@@ -73,6 +73,12 @@ int dmlp_net_info(dmlp_net *net, int32_t *residency, int32_t *n_ctas, int32_t *t
  * (n_layers entries; the output layer's column tile is always in smem). */
 int dmlp_net_layer_residency(dmlp_net *net, int32_t *where);
 
+/* Per weight layer, how many of the `fi+1` columns of every owned row sit in
+ * registers (reg_cols) and in the register plan's shared-memory tail
+ * (tail_cols); both 0 for smem / L2 layers.  For the hybrid roofline
+ * (bench.py: bytes per level / that level's peak). */
+int dmlp_net_layer_regcols(dmlp_net *net, int32_t *reg_cols, int32_t *tail_cols);
+
 /* Pack one layer from the reference layout (fo, fi+1) row-major, bias last
  * (network.py:61-64), host or device pointer, n = fo*(fi+1) floats. */
 int dmlp_net_set_layer(dmlp_net *net, int32_t layer, const float *w, int64_t n);

@@ -527,6 +527,21 @@ int dmlp_net_layer_residency(dmlp_net* net, int32_t* where) {
   return DMLP_OK;
 }
 
+int dmlp_net_layer_regcols(dmlp_net* net, int32_t* reg_cols, int32_t* tail_cols) {
+  if (!net || !reg_cols || !tail_cols) return set_error(DMLP_EINVAL, "null argument");
+  const TrainVariant* vars = nullptr;
+  train_variants(&vars);
+  const TrainVariant& tv = vars[net->variant];
+  for (int l = 0; l < net->dev.L; l++) {
+    const LayerDev& ly = net->dev.ly[l];
+    const bool reg = l < net->dev.L - 1 && ly.res == kResReg;
+    const int fi1 = ly.fi + 1;
+    reg_cols[l] = reg ? min(fi1, kThreads * tv.rc) : 0;
+    tail_cols[l] = reg ? min(fi1, kThreads * (tv.rc + tv.rs)) - reg_cols[l] : 0;
+  }
+  return DMLP_OK;
+}
+
 int dmlp_net_profile(dmlp_net* net, int32_t enable) {
   if (!net) return set_error(DMLP_EINVAL, "null net");
   DeviceGuard dg(net->device);

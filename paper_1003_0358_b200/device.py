@@ -62,6 +62,13 @@ class DeviceNet:
         #: per weight layer: "l2" (streamed every sample), "smem" or "reg" (register file)
         self.layer_residency = [("l2", "smem", "reg")[where[i]]
                                 for i in range(len(self.layer_sizes) - 1)]
+        rc = (ctypes.c_int32 * len(self.layer_sizes))()
+        tc = (ctypes.c_int32 * len(self.layer_sizes))()
+        _lib.check(_lib.lib().dmlp_net_layer_regcols(self._h, rc, tc), "dmlp_net_layer_regcols")
+        #: per weight layer: columns of every owned row held in registers / in
+        #: the register plan's shared-memory tail (0 unless "reg")
+        self.layer_reg_cols = [int(rc[i]) for i in range(len(self.layer_sizes) - 1)]
+        self.layer_tail_cols = [int(tc[i]) for i in range(len(self.layer_sizes) - 1)]
 
     # -- lifetime ---------------------------------------------------------------
     def close(self):

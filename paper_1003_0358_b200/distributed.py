@@ -91,9 +91,23 @@ def eval_counts_sharded(dev_net, x, labels, group=None):
     return allreduce_counts(counts, group)
 
 
+def _backend(group=None) -> str:
+    return str(_dist().get_backend(group)).lower()
+
+
+def _global(rank: int, group=None) -> int:
+    """Group rank -> global rank (torch.distributed src/dst arguments)."""
+    return rank if group is None else _dist().get_global_rank(group, rank)
+
+
 def broadcast_layers(dev_net, src: int = 0, group=None) -> None:
     """Broadcast the device weights of `dev_net` on rank `src` to every rank's
-    dev_net (layer by layer, device to device)."""
+    dev_net (layer by layer, device to device).
+
+    dmlp_net_get_layer / dmlp_net_set_layer run on the net's own stream while
+    torch allocates and broadcasts on its current stream, so the current
+    stream is drained before the library writes a freshly allocated tensor
+    and before it reads a received one."""
     import torch
 
     from . import _lib
@@ -101,15 +115,80 @@ def broadcast_layers(dev_net, src: int = 0, group=None) -> None:
     rank, world = world_info(group)
     if world == 1:
         return
+    cur = torch.cuda.current_stream(dev_net.device)
     for li, (fo, fi1) in enumerate(dev_net.shapes):
         t = torch.empty((fo, fi1), dtype=torch.float32, device=f"cuda:{dev_net.device}")
         if rank == src:
+            cur.synchronize()  # t's block may still be in use by queued torch work
             _lib.check(_lib.lib().dmlp_net_get_layer(dev_net._h, li, ctypes.c_void_p(t.data_ptr()),
                                                      t.numel()), "dmlp_net_get_layer")
-        _dist().broadcast(t, src=src, group=group)
+        _dist().broadcast(t, src=_global(src, group), group=group)
         if rank != src:
+            cur.synchronize()  # the broadcast landed before the library reads t
             _lib.check(_lib.lib().dmlp_net_set_layer(dev_net._h, li, ctypes.c_void_p(t.data_ptr()),
                                                      t.numel()), "dmlp_net_set_layer")
+
+
+def peer_shard(n: int, rank: int, world: int, lead: int = 0) -> tuple[int, int]:
+    """The images rank `rank` deforms when every rank except `lead` (the
+    trainer) deforms: the non-lead ranks split [0, n) in rank order."""
+    if world == 1:
+        return 0, n
+    if rank == lead:
+        return 0, 0
+    k = rank - (rank > lead)
+    return shard_range(n, k, world - 1)
+
+
+def deform_to_lead(raw, labels, params, seed: int, epoch: int, out, lead: int = 0, group=None):
+    """Peer-GPU deformation of one epoch: every rank
+    except `lead` deforms its peer_shard of the split (resident on every rank)
+    and sends it to the lead, which receives into `out` (n, 841).
+
+    Collective over `group`.  NCCL: point-to-point over NVLink; the lead's
+    receives are queued behind its current stream (the training launch), so
+    the peers deform while the lead trains and the transfer follows the
+    training kernel.  gloo (tests): staged through host memory.  Returns the
+    list of requests the lead must wait on (empty elsewhere)."""
+    import torch
+
+    from .deform import deform_device
+
+    dist = _dist()
+    rank, world = world_info(group)
+    n = int(raw.shape[0])
+    if world == 1:
+        deform_device(raw, labels, params, seed, epoch, out=out)
+        return []
+    gloo = _backend(group) == "gloo"
+    if rank != lead:
+        lo, hi = peer_shard(n, rank, world, lead)
+        if hi <= lo:
+            return []
+        shard = deform_device(raw[lo:hi], labels[lo:hi], params, seed, epoch, first=lo)
+        if gloo:
+            dist.send(shard.cpu(), dst=_global(lead, group), group=group)
+            return []
+        reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, shard, _global(lead, group),
+                                                  group)])
+        for r in reqs:
+            r.wait()
+        torch.cuda.current_stream(shard.device).synchronize()  # shard stays alive until sent
+        return []
+    ops, staged = [], []
+    for r in range(world):
+        lo, hi = peer_shard(n, r, world, lead)
+        if r == lead or hi <= lo:
+            continue
+        if gloo:
+            host = torch.empty((hi - lo, out.shape[1]), dtype=out.dtype)
+            dist.recv(host, src=_global(r, group), group=group)
+            staged.append((lo, hi, host))
+        else:
+            ops.append(dist.P2POp(dist.irecv, out[lo:hi], _global(r, group), group))
+    for lo, hi, host in staged:
+        out[lo:hi].copy_(host)
+    return dist.batch_isend_irecv(ops) if ops else []
 
 
 def counts_to_report(counts) -> dict:

@@ -51,13 +51,57 @@ def _device_eval(mlp: Mlp, images: np.ndarray, labels: np.ndarray, want_guess: b
     return x, counts, guess
 
 
-def evaluate(mlp: Mlp, test: Dataset) -> EvalReport:
+def evaluate(mlp: Mlp, test: Dataset, group=None) -> EvalReport:
+    """eval_report.py:36-67.  With a torch.distributed `group` (e.g.
+    torch.distributed.group.WORLD) this is evaluate_sharded: every rank of the
+    group must call it.  group None: this GPU alone."""
+    if group is not None:
+        return evaluate_sharded(mlp, test, group)
     n = len(test)
     if n == 0:
         return EvalReport(0.0, [], np.zeros((10, 10), dtype=np.int64), 0, 0)
     x, counts, guess = _device_eval(mlp, test.images, test.labels, True)
-    c = counts.cpu().numpy()
-    g = guess.cpu().numpy()
+    return _report(x, counts.cpu().numpy(), guess.cpu().numpy(), test)
+
+
+def evaluate_sharded(mlp: Mlp, test: Dataset, group=None) -> EvalReport:
+    """evaluate() over the ranks of `group` (one process per GPU; every rank
+    calls it with the same split): rank 0's weights are broadcast, rank r
+    ranks the samples [r*n/G, (r+1)*n/G), ONE all-reduce sums the int64[102]
+    count vector, and an all-gather of the (n, 2) top-2 guesses lets every
+    rank list the misclassified samples.  Returns the same report on every
+    rank, equal to evaluate() on one GPU."""
+    import torch
+
+    from .distributed import (_dist, allreduce_counts, broadcast_layers, shard_range,
+                              world_info)
+
+    rank, world = world_info(group)
+    n = len(test)
+    if n == 0:
+        return EvalReport(0.0, [], np.zeros((10, 10), dtype=np.int64), 0, 0)
+    dev = mlp.device_net()
+    broadcast_layers(dev, src=0, group=group)
+    if rank != 0:
+        mlp.mark_device_updated()
+    d = f"cuda:{dev.device}"
+    raw = torch.from_numpy(np.ascontiguousarray(test.images, dtype=np.uint8)).to(d)
+    lab = torch.from_numpy(np.ascontiguousarray(test.labels, dtype=np.uint8)).to(d)
+    x = upscale_device(raw)
+    lo, hi = shard_range(n, rank, world)
+    width = max(shard_range(n, r, world)[1] - shard_range(n, r, world)[0] for r in range(world))
+    guess = torch.zeros((width, 2), dtype=torch.int32, device=d)
+    counts = dev.eval_counts(x[lo:hi], lab[lo:hi], guess=guess[: hi - lo])
+    allreduce_counts(counts, group)
+    parts = [torch.empty_like(guess) for _ in range(world)]
+    _dist().all_gather(parts, guess, group=group)
+    g = torch.cat([p[: shard_range(n, r, world)[1] - shard_range(n, r, world)[0]]
+                   for r, p in enumerate(parts)]).cpu().numpy()
+    return _report(x, counts.cpu().numpy(), g, test)
+
+
+def _report(x, c: np.ndarray, g: np.ndarray, test: Dataset) -> EvalReport:
+    n = len(test)
     truth = np.asarray(test.labels).astype(np.int64)
     wrong = np.nonzero(g[:, 0] != truth)[0]
     xs = x[wrong].cpu().numpy() if len(wrong) else np.empty((0, GRID * GRID), np.float32)

@@ -71,3 +71,21 @@ def test_gloo_sharded_eval_and_deform(tmp_path, world):
     full = O.deform_epoch(imgs, labs, O.DeformParams(), seed=4, epoch=1)
     assert np.array_equal(np.concatenate([r["shard"] for r in res]), full)
     assert [(int(r["lo"]), int(r["hi"])) for r in res] == [(0, 128), (128, 257)]
+
+
+def test_peer_shard_covers_split_without_lead():
+    """deform_to_lead's split: the non-lead ranks cover [0, n) in rank order,
+    disjoint; the lead deforms nothing (it trains)."""
+    from paper_1003_0358_b200.distributed import peer_shard
+
+    for n in (0, 1, 7, 301, 60000):
+        for world in (1, 2, 3, 8):
+            for lead in {0, world - 1}:
+                spans = [peer_shard(n, r, world, lead) for r in range(world)]
+                if world == 1:
+                    assert spans == [(0, n)]
+                    continue
+                assert spans[lead] == (0, 0)
+                cov = [s for r, s in enumerate(spans) if r != lead]
+                assert cov[0][0] == 0 and cov[-1][1] == n
+                assert all(a[1] == b[0] for a, b in zip(cov, cov[1:]))
