@@ -341,6 +341,7 @@ def run_gpu(args) -> dict | None:
               "images": nd, "n_gpus": world, "sharding": "image index ranges, no collective",
               "ms_per_epoch": round(dms, 3),
               "bytes_per_img": 4149, "GBs": round(4149 * nd / (dms / 1e3) / 1e9, 1)}
+    deform["roofline"] = deform_roofline(deform["imgs_per_s_per_gpu"])
 
     # ---- evaluation: validation pass over the un-deformed training images,
     # sharded by rank + one all-reduce of the counts (eval_counts_sharded)
@@ -486,6 +487,23 @@ def relaunch_under_torchrun(n: int) -> None:
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
            *sys.argv[1:]]
     os.execv(sys.executable, cmd)
+
+
+def deform_roofline(imgs_per_s: float) -> dict | None:
+    """K2 is issue-bound (profiles/ncu_deform.json): its bound is the SM issue
+    rate (148 SMs x 4 warp instructions per cycle at the max SM clock) over
+    the warp instructions one image takes in the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_deform.json")) as f:
+            ipi = json.load(f)["warp_instructions_per_unit"]
+    except Exception:
+        return None
+    mhz = float(measured_peaks().get("sm_max_mhz", 1965.0))
+    bound = 148 * 4 * mhz * 1e6 / ipi
+    return {"bound": "issue", "achieved_imgs_per_s": round(imgs_per_s, 1),
+            "peak_imgs_per_s": round(bound, 1), "frac": round(imgs_per_s / bound, 4),
+            "warp_instructions_per_img": ipi,
+            "source": "profiles/ncu_deform.json (smsp__inst_executed / images)"}
 
 
 def l2_peak() -> float | None:

@@ -3,12 +3,16 @@
 // Replaces deform.deform_epoch / deform_image (deform.py:203-247), the
 // numpy Philox substreams (rng.py:19-38) and upscale_dataset (deform.py:
 // 250-257).  One CTA deforms one image at a time (grid-stride over images):
+//   0. a CTA of 256 threads takes kImgs = 4 images at a time, every phase
+//      spread over all of them (one barrier per phase for four images);
 //   1. key = splitmix chain over (seed, 2, epoch, index); the 423 Philox4x64-10
-//      blocks the image consumes are generated in parallel (one block per
+//      blocks each image consumes are generated in parallel (one block per
 //      thread) and decoded straight into the draw map of SURVEY App. A.1;
 //   2. 28->29 re-centring upscale in float32 (deform.py:87-99);
 //   3. 21-tap Gaussian (numpy pairwise-sum normalisation) and two separable
-//      zero-padded passes per field in fp64, scipy's symmetric tap order;
+//      zero-padded passes per field in fp64, scipy's symmetric tap order: one
+//      thread per (image, field, line), the 29-sample line in registers and
+//      the 21-tap case fully unrolled, smoothed in place;
 //   4. rotation-or-shear with anisotropic scale about the centre pixel,
 //      plus the elastic field, then the bilinear warp with -1 background.
 // This translation unit is compiled with -fmad=false: the reference never
@@ -61,90 +65,146 @@ __device__ __forceinline__ double uniform(double lo, double hi, double u) {
   return lo + (hi - lo) * u;
 }
 
-struct DefSmem {
-  double nx[kPix], ny[kPix], tmp[kPix];
+// Several images per CTA (kImgs): every phase below runs over all of them at
+// once, so each barrier is shared by kImgs images and the per-image phases
+// with little parallelism (the 21 taps, the scalars) fill the CTA.
+constexpr int kImgs = 4;
+
+struct ImgSmem {
+  double nx[kPix], ny[kPix];  // noise fields, smoothed in place
   float up[kPix];
-  double g[64];
-  double u[8];  // sigma-u, alpha-u, mode, angle-u, gamma-u, sx-u, sy-u
-  double scal[6];
+  __align__(16) uint8_t raw[784];
+  double g[64];    // Gaussian taps
+  double u[8];     // sigma-u, alpha-u, mode, angle-u, gamma-u, sx-u, sy-u | tap sum
+  double scal[9];  // sigma, alpha, mode, angle, sx, sy | cos, sin, tan of the angle
   uint64_t key[2];
 };
 
-// scipy.ndimage.convolve1d, constant mode, symmetric kernel (deform.py:130-131):
-// out = x[c]*g(0) + sum_{k=h..1} (x[c-k] + x[c+k]) * g(k).
-__device__ __forceinline__ void conv_pass(const double* in, double* out, const double* g, int h,
-                                          int axis, double scale) {
-  for (int p = threadIdx.x; p < kPix; p += blockDim.x) {
-    const int r = p / kGrid, c = p % kGrid;
-    const int pos = axis == 0 ? r : c;
-    double acc = in[p] * g[h];
-    for (int k = h; k >= 1; k--) {
-      const int lo = pos - k, hi = pos + k;
-      double xl = 0.0, xh = 0.0;
-      if (lo >= 0) xl = axis == 0 ? in[lo * kGrid + c] : in[r * kGrid + lo];
-      if (hi < kGrid) xh = axis == 0 ? in[hi * kGrid + c] : in[r * kGrid + hi];
-      acc = acc + (xl + xh) * g[h + k];
+// deform.py:87-99: v / 127.5 - 1 per byte (float32, the IEEE division done
+// once per byte value into a 256-entry table), then the 2x2 mean of the
+// re-centred 29x29 grid.  img: the 784 bytes, staged in shared memory.
+__device__ __forceinline__ void byte_table(float* lut) {
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = (float)v / 127.5f - 1.0f;
+}
+__device__ __forceinline__ void upscale_px(const uint8_t* img, const float* lut, int p, float* up) {
+  const int r = p / kGrid, c = p % kGrid;
+  const int r0 = max(r - 1, 0), r1 = min(r, 27), c0 = max(c - 1, 0), c1 = min(c, 27);
+  const float n00 = lut[img[r0 * 28 + c0]];
+  const float n01 = lut[img[r0 * 28 + c1]];
+  const float n10 = lut[img[r1 * 28 + c0]];
+  const float n11 = lut[img[r1 * 28 + c1]];
+  up[p] = 0.25f * (((n00 + n01) + n10) + n11);
+}
+
+// scipy.ndimage.convolve1d, constant mode (zero padding), symmetric kernel
+// (deform.py:130-131), along one 29-sample line held in registers:
+// out[c] = x[c]*g(0) + sum_{k=h..1} (x[c-k] + x[c+k]) * g(k), with the
+// out-of-range samples as explicit zeros (the same additions as scipy).
+// H = the half width at compile time (fully unrolled, taps in registers);
+// H < 0: the half width h at run time (any odd kernel size).
+template <int H>
+__device__ __forceinline__ void conv_line(double* base, int stride, bool act, const double* gs,
+                                          int h) {
+  double x[kGrid];
+#pragma unroll
+  for (int i = 0; i < kGrid; i++) x[i] = act ? base[i * stride] : 0.0;
+  __syncthreads();  // every line of the pass is read before any is overwritten
+  if (!act) return;
+  if constexpr (H >= 0) {
+    double g[H + 1];  // g[k] = tap at distance k
+#pragma unroll
+    for (int k = 0; k <= H; k++) g[k] = gs[H + k];
+#pragma unroll
+    for (int c = 0; c < kGrid; c++) {
+      double acc = x[c] * g[0];
+#pragma unroll
+      for (int k = H; k >= 1; k--) {
+        const double xl = c - k >= 0 ? x[c - k >= 0 ? c - k : 0] : 0.0;
+        const double xh = c + k < kGrid ? x[c + k < kGrid ? c + k : 0] : 0.0;
+        acc = acc + (xl + xh) * g[k];
+      }
+      base[c * stride] = acc;
     }
-    out[p] = scale == 0.0 ? acc : scale * acc;
+  } else {
+    for (int c = 0; c < kGrid; c++) {
+      double acc = x[c] * gs[h];
+      for (int k = h; k >= 1; k--) {
+        const double xl = c - k >= 0 ? x[c - k] : 0.0;
+        const double xh = c + k < kGrid ? x[c + k] : 0.0;
+        acc = acc + (xl + xh) * gs[h + k];
+      }
+      base[c * stride] = acc;
+    }
   }
 }
 
-__device__ __forceinline__ void upscale_img(const uint8_t* img, float* up) {
-  for (int p = threadIdx.x; p < kPix; p += blockDim.x) {
-    const int r = p / kGrid, c = p % kGrid;
-    const int r0 = max(r - 1, 0), r1 = min(r, 27), c0 = max(c - 1, 0), c1 = min(c, 27);
-    const float n00 = (float)img[r0 * 28 + c0] / 127.5f - 1.0f;
-    const float n01 = (float)img[r0 * 28 + c1] / 127.5f - 1.0f;
-    const float n10 = (float)img[r1 * 28 + c0] / 127.5f - 1.0f;
-    const float n11 = (float)img[r1 * 28 + c1] / 127.5f - 1.0f;
-    up[p] = 0.25f * (((n00 + n01) + n10) + n11);
-  }
-}
-
-// Full pipeline for one image given the draws in S (noise in nx/ny, scalars in scal).
-__device__ void deform_from_draws(DefSmem& S, int ks, float* out) {
+// The smoothing and the warp of up to kImgs images whose draws are in S[]
+// (noise in nx/ny, scalars in scal[0..5]); out rows of kPix floats.
+template <int H>
+__device__ __forceinline__ void deform_batch(ImgSmem* S, int nimg, int ks, float* out) {
   const int tid = threadIdx.x;
-  const double sigma = S.scal[0], alpha = S.scal[1];
   const int h = ks / 2;
-  if (tid < ks) {
-    const double off = (double)tid - (double)h;
-    S.g[tid] = exp(-(off * off) / (2.0 * sigma * sigma));
+  // taps (64 threads per image) and the rotation's trig (one thread per image)
+  {
+    const int i = tid >> 6, j = tid & 63;
+    if (i < nimg) {
+      const double sigma = S[i].scal[0];
+      if (j < ks) {
+        const double off = (double)j - (double)h;
+        S[i].g[j] = exp(-(off * off) / (2.0 * sigma * sigma));
+      }
+      if (j == 63) {
+        const double rad = S[i].scal[3] * (3.141592653589793 / 180.0);  // np.deg2rad
+        S[i].scal[6] = cos(rad);
+        S[i].scal[7] = sin(rad);
+        S[i].scal[8] = tan(rad);
+      }
+    }
   }
   __syncthreads();
-  if (tid == 0) {  // numpy pairwise sum of the taps (n < 128 branch)
-    double s;
+  if ((tid & 63) == 0 && (tid >> 6) < nimg) {  // numpy pairwise sum of the taps (n < 128)
+    const double* g = S[tid >> 6].g;
+    double sum;
     if (ks < 8) {
-      s = 0.0;
-      for (int i = 0; i < ks; i++) s += S.g[i];
+      sum = 0.0;
+      for (int i = 0; i < ks; i++) sum += g[i];
     } else {
       double r[8];
-      for (int k = 0; k < 8; k++) r[k] = S.g[k];
+      for (int k = 0; k < 8; k++) r[k] = g[k];
       int i;
       for (i = 8; i < ks - (ks % 8); i += 8)
-        for (int k = 0; k < 8; k++) r[k] += S.g[i + k];
-      s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-      for (; i < ks; i++) s += S.g[i];
+        for (int k = 0; k < 8; k++) r[k] += g[i + k];
+      sum = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      for (; i < ks; i++) sum += g[i];
     }
-    S.u[7] = s;
+    S[tid >> 6].u[7] = sum;
   }
   __syncthreads();
-  if (tid < ks) S.g[tid] = S.g[tid] / S.u[7];
+  {
+    const int i = tid >> 6, j = tid & 63;
+    if (i < nimg && j < ks) S[i].g[j] = S[i].g[j] / S[i].u[7];
+  }
   __syncthreads();
-  conv_pass(S.nx, S.tmp, S.g, h, 0, 0.0);
+  // separable passes: axis 0 (down the columns) then axis 1 (along the rows),
+  // one thread per (image, field, line), the line in registers
+  const int nl = nimg * 2 * kGrid;
+  const bool act = tid < nl;
+  const int i = act ? tid / (2 * kGrid) : 0, f = (tid / kGrid) & 1, line = tid % kGrid;
+  double* fld = f ? S[i].ny : S[i].nx;
+  conv_line<H>(fld + line, kGrid, act, S[i].g, h);  // column `line`
   __syncthreads();
-  conv_pass(S.tmp, S.nx, S.g, h, 1, 0.0);
+  conv_line<H>(fld + line * kGrid, 1, act, S[i].g, h);  // row `line`
   __syncthreads();
-  conv_pass(S.ny, S.tmp, S.g, h, 0, 0.0);
-  __syncthreads();
-  conv_pass(S.tmp, S.ny, S.g, h, 1, 0.0);
-  __syncthreads();
-
-  const int mode = (int)S.scal[2];
-  const double angle = S.scal[3], sx = S.scal[4], sy = S.scal[5];
-  const double rad = angle * (3.141592653589793 / 180.0);  // np.deg2rad
-  const double cs = cos(rad), sn = sin(rad), tn = tan(rad);
+  // rotation-or-shear + scale about the centre, plus the elastic field, then
+  // the bilinear warp with -1 background and clip (deform.py:170-200)
   const double center = (kGrid - 1) / 2.0;
-  for (int p = tid; p < kPix; p += blockDim.x) {
+  for (int t = tid; t < nimg * kPix; t += blockDim.x) {
+    const int im = t / kPix, p = t - im * kPix;
+    const ImgSmem& Si = S[im];
+    const double alpha = Si.scal[1];
+    const int mode = (int)Si.scal[2];
+    const double sx = Si.scal[4], sy = Si.scal[5];
+    const double cs = Si.scal[6], sn = Si.scal[7], tn = Si.scal[8];
     const int r = p / kGrid, c = p % kGrid;
     const double y = (double)r - center, x = (double)c - center;
     const double xs = sx * x, ys = sy * y;
@@ -156,8 +216,8 @@ __device__ void deform_from_draws(DefSmem& S, int ks, float* out) {
       xr = xs + tn * ys;
       yr = ys;
     }
-    const double dx = (xr - x) + alpha * S.nx[p];
-    const double dy = (yr - y) + alpha * S.ny[p];
+    const double dx = (xr - x) + alpha * Si.nx[p];
+    const double dy = (yr - y) + alpha * Si.ny[p];
     const double sr = (double)r + dy, sc = (double)c + dx;
     const double flr = floor(sr), flc = floor(sc);
     const long long i0 = (long long)flr, j0 = (long long)flc;
@@ -167,111 +227,150 @@ __device__ void deform_from_draws(DefSmem& S, int ks, float* out) {
     for (int q = 0; q < 4; q++) {
       const long long ii = i0 + (q >> 1), jj = j0 + (q & 1);
       const bool valid = ii >= 0 && ii < kGrid && jj >= 0 && jj < kGrid;
-      v[q] = valid ? (double)S.up[ii * kGrid + jj] : -1.0;
+      v[q] = valid ? (double)Si.up[ii * kGrid + jj] : -1.0;
     }
     double o = (1.0 - fr) * (1.0 - fc) * v[0];
     o = o + (1.0 - fr) * fc * v[1];
     o = o + fr * (1.0 - fc) * v[2];
     o = o + fr * fc * v[3];
     o = o < -1.0 ? -1.0 : (o > 1.0 ? 1.0 : o);
-    out[p] = (float)o;
+    out[(size_t)im * kPix + p] = (float)o;
   }
 }
 
-__global__ void __launch_bounds__(kDefThreads, 4)
+template <int H>
+__global__ void __launch_bounds__(kDefThreads, 2)
     k_deform(const uint8_t* __restrict__ raw, const uint8_t* __restrict__ labels, long long first,
              long long n, unsigned long long seed, unsigned long long epoch, DefP P,
              float* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  DefSmem& S = *reinterpret_cast<DefSmem*>(smraw);
+  ImgSmem* S = reinterpret_cast<ImgSmem*>(smraw);
+  float* lut = reinterpret_cast<float*>(S + kImgs);
   const int tid = threadIdx.x;
   const int N = kPix;
-  for (long long img = blockIdx.x; img < n; img += gridDim.x) {
-    if (tid == 0) {
+  byte_table(lut);
+  for (long long b0 = (long long)blockIdx.x * kImgs; b0 < n; b0 += (long long)gridDim.x * kImgs) {
+    const int nimg = (int)min((long long)kImgs, n - b0);
+    if (tid < nimg) {  // substream key (seed, 2, epoch, index), rng.py:27-38
       uint64_t hh = splitmix64(seed);
       hh = splitmix64(hh ^ 2ULL);
       hh = splitmix64(hh ^ epoch);
-      hh = splitmix64(hh ^ (uint64_t)(first + img));
-      S.key[0] = hh;
-      S.key[1] = splitmix64(hh);
+      hh = splitmix64(hh ^ (uint64_t)(first + b0 + tid));
+      S[tid].key[0] = hh;
+      S[tid].key[1] = splitmix64(hh);
     }
-    upscale_img(raw + img * 784, S.up);
+    if ((reinterpret_cast<uintptr_t>(raw) & 15) == 0) {  // raw bytes as 16-byte vectors (784 = 49*16)
+      for (int t = tid; t < nimg * 49; t += blockDim.x) {
+        const int im = t / 49;
+        reinterpret_cast<uint4*>(S[im].raw)[t - im * 49] =
+            reinterpret_cast<const uint4*>(raw + (b0 + im) * 784)[t - im * 49];
+      }
+    } else {
+      for (int t = tid; t < nimg * 784; t += blockDim.x) S[t / 784].raw[t % 784] = raw[b0 * 784 + t];
+    }
     __syncthreads();
-    const uint64_t k0 = S.key[0], k1 = S.key[1];
-    for (int b = tid; b < kBlocks; b += blockDim.x) {
+    for (int t = tid; t < nimg * kPix; t += blockDim.x) {
+      const int im = t / kPix;
+      upscale_px(S[im].raw, lut, t - im * kPix, S[im].up);
+    }
+    // the 423 Philox4x64-10 blocks of every image, decoded into the draw map
+    // (two blocks per thread interleaved measured slower: 47.0 -> 45.1M imgs/s)
+    for (int t = tid; t < nimg * kBlocks; t += blockDim.x) {
+      const int im = t / kBlocks, b = t - im * kBlocks;
+      ImgSmem& Si = S[im];
       uint64_t w[4];
-      philox4x64_10(k0, k1, (uint64_t)b + 1, w);
+      philox4x64_10(Si.key[0], Si.key[1], (uint64_t)b + 1, w);
 #pragma unroll
       for (int e = 0; e < 4; e++) {
         const int wi = 4 * b + e;
         if (wi >= kWords) break;
         if (wi >= 2 && wi < 2 + N) {
-          S.nx[wi - 2] = uniform(-1.0, 1.0, u53(w[e]));
+          Si.nx[wi - 2] = uniform(-1.0, 1.0, u53(w[e]));
         } else if (wi >= 2 + N && wi < 2 + 2 * N) {
-          S.ny[wi - 2 - N] = uniform(-1.0, 1.0, u53(w[e]));
+          Si.ny[wi - 2 - N] = uniform(-1.0, 1.0, u53(w[e]));
         } else if (wi == 2 + 2 * N) {  // integers(0, 2): bit 31 of the low half
-          S.u[2] = (double)(((w[e] & 0xFFFFFFFFULL) * 2ULL) >> 32);
+          Si.u[2] = (double)(((w[e] & 0xFFFFFFFFULL) * 2ULL) >> 32);
         } else {
           const int slot = wi < 2 ? wi : wi - 2 * N;  // 0,1 | 3..6
-          S.u[slot] = u53(w[e]);
+          Si.u[slot] = u53(w[e]);
         }
       }
     }
     __syncthreads();
-    if (tid == 0) {
-      const int digit = labels[img];
+    if (tid < nimg) {
+      ImgSmem& Si = S[tid];
+      const int digit = labels[b0 + tid];
       const double beta = (digit == 1 || digit == 7) ? P.beta_red : P.beta_def;
-      S.scal[0] = uniform(P.sig_lo, P.sig_hi, S.u[0]);
-      S.scal[1] = uniform(P.al_lo, P.al_hi, S.u[1]);
-      S.scal[2] = S.u[2];
-      S.scal[3] = uniform(-beta, beta, S.u[3]);
-      const double gamma = uniform(P.ga_lo, P.ga_hi, S.u[4]);
-      S.scal[4] = uniform(1.0 - gamma / 100.0, 1.0 + gamma / 100.0, S.u[5]);
-      S.scal[5] = uniform(1.0 - gamma / 100.0, 1.0 + gamma / 100.0, S.u[6]);
+      Si.scal[0] = uniform(P.sig_lo, P.sig_hi, Si.u[0]);
+      Si.scal[1] = uniform(P.al_lo, P.al_hi, Si.u[1]);
+      Si.scal[2] = Si.u[2];
+      Si.scal[3] = uniform(-beta, beta, Si.u[3]);
+      const double gamma = uniform(P.ga_lo, P.ga_hi, Si.u[4]);
+      Si.scal[4] = uniform(1.0 - gamma / 100.0, 1.0 + gamma / 100.0, Si.u[5]);
+      Si.scal[5] = uniform(1.0 - gamma / 100.0, 1.0 + gamma / 100.0, Si.u[6]);
     }
     __syncthreads();
-    deform_from_draws(S, P.ks, out + img * kPix);
+    deform_batch<H>(S, nimg, P.ks, out + b0 * kPix);
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kDefThreads, 4)
+template <int H>
+__global__ void __launch_bounds__(kDefThreads, 2)
     k_deform_injected(const uint8_t* __restrict__ raw, long long n, const double* __restrict__ ndx,
                       const double* __restrict__ ndy, const double* __restrict__ scal, int ks,
                       float* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  DefSmem& S = *reinterpret_cast<DefSmem*>(smraw);
+  ImgSmem* S = reinterpret_cast<ImgSmem*>(smraw);
+  float* lut = reinterpret_cast<float*>(S + kImgs);
   const int tid = threadIdx.x;
-  for (long long img = blockIdx.x; img < n; img += gridDim.x) {
-    upscale_img(raw + img * 784, S.up);
-    for (int p = tid; p < kPix; p += blockDim.x) {
-      S.nx[p] = ndx[img * kPix + p];
-      S.ny[p] = ndy[img * kPix + p];
-    }
-    if (tid < 6) S.scal[tid] = scal[img * 6 + tid];
+  byte_table(lut);
+  for (long long b0 = (long long)blockIdx.x * kImgs; b0 < n; b0 += (long long)gridDim.x * kImgs) {
+    const int nimg = (int)min((long long)kImgs, n - b0);
+    for (int t = tid; t < nimg * 784; t += blockDim.x) S[t / 784].raw[t % 784] = raw[b0 * 784 + t];
     __syncthreads();
-    deform_from_draws(S, ks, out + img * kPix);
+    for (int t = tid; t < nimg * kPix; t += blockDim.x) {
+      const int im = t / kPix, p = t - im * kPix;
+      upscale_px(S[im].raw, lut, p, S[im].up);
+      S[im].nx[p] = ndx[(b0 + im) * kPix + p];
+      S[im].ny[p] = ndy[(b0 + im) * kPix + p];
+    }
+    if (tid < 6 * nimg) S[tid / 6].scal[tid % 6] = scal[b0 * 6 + tid];
+    __syncthreads();
+    deform_batch<H>(S, nimg, ks, out + b0 * kPix);
     __syncthreads();
   }
 }
 
 __global__ void k_upscale(const uint8_t* __restrict__ raw, long long n, float* __restrict__ out) {
-  __shared__ float up[kPix];
-  for (long long img = blockIdx.x; img < n; img += gridDim.x) {
-    upscale_img(raw + img * 784, up);
+  __shared__ float lut[256];
+  __shared__ __align__(16) uint8_t img[784];
+  byte_table(lut);
+  for (long long i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int t = threadIdx.x; t < 784; t += blockDim.x) img[t] = raw[i * 784 + t];
     __syncthreads();
-    for (int p = threadIdx.x; p < kPix; p += blockDim.x) out[img * kPix + p] = up[p];
+    for (int p = threadIdx.x; p < kPix; p += blockDim.x) {
+      const int r = p / kGrid, c = p % kGrid;
+      const int r0 = max(r - 1, 0), r1 = min(r, 27), c0 = max(c - 1, 0), c1 = min(c, 27);
+      out[i * kPix + p] = 0.25f * (((lut[img[r0 * 28 + c0]] + lut[img[r0 * 28 + c1]]) +
+                                    lut[img[r1 * 28 + c0]]) + lut[img[r1 * 28 + c1]]);
+    }
     __syncthreads();
   }
 }
 
-static int grid_for(long long n) {
+static int grid_for(long long n, int per_cta = 1, int per_sm = 8) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long g = (long long)sms * 8;
-  return (int)(n < g ? n : g);
+  const long long units = (n + per_cta - 1) / per_cta;
+  const long long g = (long long)sms * per_sm;
+  return (int)(units < g ? units : g);
 }
+
+// The compiled half width of the fully unrolled smoothing (kernel_size 21,
+// deform.py's default); other sizes run the run-time-width instance.
+constexpr int kUnrolledH = 10;
 
 static int check_params(const dmlp_deform_params* p) {
   auto bad = [](double lo, double hi) { return !(isfinite(lo) && isfinite(hi)) || lo > hi; };
@@ -305,11 +404,12 @@ int dmlp_deform(const uint8_t* raw_dev, const uint8_t* labels_dev, int64_t first
   DefP P{params->sigma_lo,     params->sigma_hi,     params->alpha_lo, params->alpha_hi,
          params->beta_default, params->beta_reduced, params->gamma_lo, params->gamma_hi,
          params->kernel_size};
-  const int smem = (int)sizeof(DefSmem);
-  rc = cuda_check(cudaFuncSetAttribute(k_deform, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+  const int smem = (int)sizeof(ImgSmem) * kImgs + 256 * (int)sizeof(float);
+  auto fn = params->kernel_size == 2 * kUnrolledH + 1 ? k_deform<kUnrolledH> : k_deform<-1>;
+  rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                   "cudaFuncSetAttribute");
   if (rc) return rc;
-  k_deform<<<grid_for(n), kDefThreads, smem, (cudaStream_t)stream>>>(
+  fn<<<grid_for(n, kImgs, 2), kDefThreads, smem, (cudaStream_t)stream>>>(
       raw_dev, labels_dev, first, n, seed, epoch, P, out_dev);
   return cuda_check(cudaGetLastError(), "k_deform");
 }
@@ -322,12 +422,13 @@ int dmlp_deform_injected(const uint8_t* raw_dev, int64_t n, const double* noise_
   if (n <= 0) return DMLP_OK;
   if (!raw_dev || !noise_dx_dev || !noise_dy_dev || !scalars_dev || !out_dev)
     return set_error(DMLP_EINVAL, "null argument");
-  const int smem = (int)sizeof(DefSmem);
-  int rc = cuda_check(
-      cudaFuncSetAttribute(k_deform_injected, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-      "cudaFuncSetAttribute");
+  const int smem = (int)sizeof(ImgSmem) * kImgs + 256 * (int)sizeof(float);
+  auto fn = kernel_size == 2 * kUnrolledH + 1 ? k_deform_injected<kUnrolledH>
+                                              : k_deform_injected<-1>;
+  int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                      "cudaFuncSetAttribute");
   if (rc) return rc;
-  k_deform_injected<<<grid_for(n), kDefThreads, smem, (cudaStream_t)stream>>>(
+  fn<<<grid_for(n, kImgs, 2), kDefThreads, smem, (cudaStream_t)stream>>>(
       raw_dev, n, noise_dx_dev, noise_dy_dev, scalars_dev, kernel_size, out_dev);
   return cuda_check(cudaGetLastError(), "k_deform_injected");
 }

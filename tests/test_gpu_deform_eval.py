@@ -121,3 +121,18 @@ def test_eval_big_nets_vs_oracle(sizes):
     # bounded; argmax must agree on every other sample
     assert int((~ok).sum()) <= len(ok) // 200, f"{int((~ok).sum())} near ties"
     assert np.array_equal(np.argmax(out, 1)[ok], np.argmax(ref, 1)[ok])
+
+
+@pytest.mark.parametrize("ks", [3, 7, 63])
+def test_deform_other_kernel_sizes_vs_oracle(ks):
+    """Kernel sizes other than the default 21 run the run-time-width
+    smoothing (deform_kernel.cu conv_line<-1>); batches of 1..4 images per
+    CTA (n = 13 leaves a ragged last batch)."""
+    from paper_1003_0358_b200.deform import DeformParams, deform_device
+    from paper_1003_0358_b200.synthetic import make_digits
+
+    imgs, labs = make_digits(13, seed=5)
+    ref = O.deform_epoch(imgs, labs, O.DeformParams(kernel_size=ks), seed=2, epoch=1)
+    out = deform_device(_cuda(imgs), _cuda(labs), DeformParams(kernel_size=ks), 2, 1)
+    d = np.abs(out.cpu().numpy().reshape(-1, 29, 29) - ref)
+    assert d.max() <= 1e-5, d.max()
