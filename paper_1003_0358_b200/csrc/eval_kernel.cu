@@ -4,8 +4,8 @@
 // (network.py:133-135), trainer.error_percent (trainer.py:90-96) and the
 // counting of eval_report.evaluate (eval_report.py:36-67).
 //   * hidden layers: fp32 SIMT GEMM (128x128 CTA tile, 8x8 per thread,
-//     double-buffered smem) with the bias add and the scaled tanh fused in
-//     the epilogue.  fp32 accumulation keeps argmax parity with the
+//     double-buffered smem, float4 row loads transposed into k-major tiles)
+//     with the bias add and the scaled tanh fused in the epilogue.  fp32 accumulation keeps argmax parity with the
 //     reference's OpenBLAS sgemm; tensor-core tf32 would not.
 //   * output layer: one warp per sample (10 rows, weights in smem), fused
 //     with stable top-2 ranking and the {wrong, confusion, second-guess}
@@ -22,7 +22,17 @@ namespace dmlp {
 constexpr int BM = 128, BN = 128, BK = 16, GT = 256;
 
 // Y[m][j] = A*tanh(B*(sum_k X[m][k] W[j][k] + W[j][K])), m < M, j < N.
-__global__ void __launch_bounds__(GT)
+// 128x128 CTA tile, 8x8 outer products per thread over k-major smem tiles
+// (As[k][m], Bs[k][n]: one LDS.128 per 4 fragment values), double-buffered
+// smem fed from registers.  The global loads are row-major float4s (VEC:
+// rows 16-byte aligned, ld % 4 == 0; else scalar): thread t loads row
+// t % 128, k-half t / 128 of both tiles, so every warp stores 32 consecutive
+// m (or n) of one k row -- conflict-free transposes (C4 33.2 -> 36.7 TFLOP/s;
+// a 3-stage pipeline of transposing 4-byte cp.async measured 27.8, and one
+// CTA per SM with more registers 34.6).  Thread (ty, tx) owns rows
+// ty*4 + {0..3, 64..67} and columns tx*4 + {0..3, 64..67}.
+template <bool VEC>
+__global__ void __launch_bounds__(GT, 2)
     k_gemm_tanh(const float* __restrict__ X, long long ldx, const float* __restrict__ W, int ldw,
                 int M, int N, int K, float* __restrict__ Y, int ldy) {
   __shared__ __align__(16) float As[2][BK][BM];
@@ -30,16 +40,30 @@ __global__ void __launch_bounds__(GT)
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
-  // loader mapping: 128 rows x 16 k = 2048 floats, 8 per thread: row = tid/2, k = (tid&1)*8 + e
-  const int lr = tid >> 1, lk = (tid & 1) * 8;
+  const int lr = tid & 127, lk = (tid >> 7) * 8;  // loader: row, first of 8 k
+  const bool am = bm + lr < M, bnv = bn + lr < N;
+  const float* xa = X + (long long)(am ? bm + lr : 0) * ldx;
+  const float* wb = W + (long long)(bnv ? bn + lr : 0) * ldw;
   float ra[8], rb[8];
   auto load = [&](int k0) {
-    const int m = bm + lr, j = bn + lr;
+    const int kb = k0 + lk;
+    if (VEC && kb + 8 <= K) {
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 a0 = am ? *reinterpret_cast<const float4*>(xa + kb) : z;
+      const float4 a1 = am ? *reinterpret_cast<const float4*>(xa + kb + 4) : z;
+      const float4 b0 = bnv ? __ldg(reinterpret_cast<const float4*>(wb + kb)) : z;
+      const float4 b1 = bnv ? __ldg(reinterpret_cast<const float4*>(wb + kb + 4)) : z;
+      ra[0] = a0.x; ra[1] = a0.y; ra[2] = a0.z; ra[3] = a0.w;
+      ra[4] = a1.x; ra[5] = a1.y; ra[6] = a1.z; ra[7] = a1.w;
+      rb[0] = b0.x; rb[1] = b0.y; rb[2] = b0.z; rb[3] = b0.w;
+      rb[4] = b1.x; rb[5] = b1.y; rb[6] = b1.z; rb[7] = b1.w;
+    } else {
 #pragma unroll
-    for (int e = 0; e < 8; e++) {
-      const int k = k0 + lk + e;
-      ra[e] = (m < M && k < K) ? X[(long long)m * ldx + k] : 0.0f;
-      rb[e] = (j < N && k < K) ? W[(long long)j * ldw + k] : 0.0f;
+      for (int e = 0; e < 8; e++) {
+        const int k = kb + e;
+        ra[e] = (am && k < K) ? xa[k] : 0.0f;
+        rb[e] = (bnv && k < K) ? __ldg(wb + k) : 0.0f;
+      }
     }
   };
   auto store = [&](int b) {
@@ -87,7 +111,7 @@ __global__ void __launch_bounds__(GT)
     for (int j = 0; j < 8; j++) {
       const int n = bn + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
       if (n >= N) continue;
-      const float a = acc[i][j] + W[(long long)n * ldw + K];
+      const float a = acc[i][j] + __ldg(W + (long long)n * ldw + K);
       float t;
       Y[(long long)m * ldy + n] = dev_scaled_tanh(a, &t);
     }
@@ -205,8 +229,9 @@ static int run_eval(dmlp_net* net, const float* x, long long n, float* out, cons
       float* y = net->d_act[b];
       const int ldy = net->hl[l + 1].pitch;
       dim3 grid((h.fo + BN - 1) / BN, (M + BM - 1) / BM);
-      k_gemm_tanh<<<grid, GT, 0, st>>>(in, ldin, net->d_w + h.w_off, h.pitch, M, h.fo, h.fi, y,
-                                        ldy);
+      const bool vec = ldin % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+      (vec ? k_gemm_tanh<true> : k_gemm_tanh<false>)<<<grid, GT, 0, st>>>(
+          in, ldin, net->d_w + h.w_off, h.pitch, M, h.fo, h.fi, y, ldy);
       in = y;
       ldin = ldy;
       b ^= 1;
