@@ -199,3 +199,52 @@ def test_resume_from_interrupt_checkpoint(tmp_path, monkeypatch):
     assert [h.epoch for h in rest.history] == [1, 2]
     for a, b in zip(rest.history, full.history[1:]):
         assert (a.train_error, a.val_error) == (b.train_error, b.val_error)
+
+
+def test_load_dataset_device_matches_host(tmp_path):
+    """IDX ingestion straight into HBM (mnist_io.load_dataset_device) holds the
+    same bytes as the host parser, and raises the same errors."""
+    import gzip
+
+    from paper_1003_0358_b200 import mnist_io
+    from paper_1003_0358_b200.synthetic import make_digits, write_idx_images, write_idx_labels
+
+    imgs, labs = make_digits(300, seed=4)
+    (tmp_path / "i.gz").write_bytes(gzip.compress(write_idx_images(imgs)))
+    (tmp_path / "l").write_bytes(write_idx_labels(labs))
+    di, dl = mnist_io.load_dataset_device(tmp_path / "i.gz", tmp_path / "l")
+    assert di.is_cuda and np.array_equal(di.cpu().numpy(), imgs)
+    assert np.array_equal(dl.cpu().numpy(), labs)
+    bad = labs.copy()
+    bad[7] = 11
+    (tmp_path / "b").write_bytes(write_idx_labels(bad))
+    with pytest.raises(mnist_io.LabelOutOfRange):
+        mnist_io.load_dataset_device(tmp_path / "i.gz", tmp_path / "b")
+    (tmp_path / "s").write_bytes(write_idx_labels(labs[:10]))
+    with pytest.raises(mnist_io.CountMismatch):
+        mnist_io.load_dataset_device(tmp_path / "i.gz", tmp_path / "s")
+
+
+def test_bench_line_smoke():
+    """bench.py end to end at a small size: one JSON line with the contract's
+    keys, the L2 roofline and the hybrid fraction, the deformation and eval
+    extras."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--config", "C1", "--samples", "3000",
+                          "--steps", "2", "--warmup", "3", "--cpu-seconds", "0",
+                          "--deform-images", "4096"], cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "config", "e2e", "gpu_launches", "roofline",
+              "clocks", "deform", "eval"):
+        assert k in line, k
+    assert line["roofline"]["bound"] == "l2" and 0 < line["roofline"]["frac"] < 1
+    assert 0 < line["roofline"]["hybrid"]["frac_hybrid"] < 1
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["deform"]["imgs_per_s"] > 0
