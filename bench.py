@@ -304,6 +304,7 @@ def run_gpu(args) -> dict | None:
     x_host.copy_(x.cpu())
     lab_host = torch.from_numpy(labels).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))
+    trainer.train_epoch(mlp, x_host, lab_host, 1e-3, rng=substream(rank, 3, 99))  # warm-up
     barrier()
     t0 = time.perf_counter()
     for s in range(e2e_steps):
