@@ -502,6 +502,7 @@ int dmlp_net_destroy(dmlp_net* net) {
   cudaFree(net->d_stage_wrong);
   cudaFree(net->d_act[0]);
   cudaFree(net->d_act[1]);
+  cudaFree(net->d_act[2]);
   cudaFree(net->dev.prof);
   cudaFree(net->dev.trace);
   if (net->stream) cudaStreamDestroy(net->stream);

@@ -101,7 +101,7 @@ struct dmlp_net {
   uint8_t* d_stage_lab = nullptr;
   long long* d_stage_wrong = nullptr;
   // evaluation scratch
-  float* d_act[2] = {nullptr, nullptr};
+  float* d_act[3] = {nullptr, nullptr, nullptr};  // layer outputs (ping-pong) | padded inputs
   size_t act_rows = 0;
   int act_ld = 0;
 };

@@ -35,64 +35,69 @@ template <bool VEC>
 __global__ void __launch_bounds__(GT, 2)
     k_gemm_tanh(const float* __restrict__ X, long long ldx, const float* __restrict__ W, int ldw,
                 int M, int N, int K, float* __restrict__ Y, int ldy) {
-  __shared__ __align__(16) float As[2][BK][BM];
-  __shared__ __align__(16) float Bs[2][BK][BN];
+  constexpr int KB = 8;  // k per smem tile
+  __shared__ __align__(16) float As[2][KB][BM];
+  __shared__ __align__(16) float Bs[2][KB][BN];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
-  const int lr = tid & 127, lk = (tid >> 7) * 8;  // loader: row, first of 8 k
+  const int lr = tid & 127, lk = (tid >> 7) * 4;  // loader: row, first of 4 k
   const bool am = bm + lr < M, bnv = bn + lr < N;
   const float* xa = X + (long long)(am ? bm + lr : 0) * ldx;
   const float* wb = W + (long long)(bnv ? bn + lr : 0) * ldw;
-  float ra[8], rb[8];
+  float4 ra, rb;
   auto load = [&](int k0) {
     const int kb = k0 + lk;
-    if (VEC && kb + 8 <= K) {
-      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 a0 = am ? *reinterpret_cast<const float4*>(xa + kb) : z;
-      const float4 a1 = am ? *reinterpret_cast<const float4*>(xa + kb + 4) : z;
-      const float4 b0 = bnv ? __ldg(reinterpret_cast<const float4*>(wb + kb)) : z;
-      const float4 b1 = bnv ? __ldg(reinterpret_cast<const float4*>(wb + kb + 4)) : z;
-      ra[0] = a0.x; ra[1] = a0.y; ra[2] = a0.z; ra[3] = a0.w;
-      ra[4] = a1.x; ra[5] = a1.y; ra[6] = a1.z; ra[7] = a1.w;
-      rb[0] = b0.x; rb[1] = b0.y; rb[2] = b0.z; rb[3] = b0.w;
-      rb[4] = b1.x; rb[5] = b1.y; rb[6] = b1.z; rb[7] = b1.w;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (VEC && kb + 4 <= K) {
+      ra = am ? *reinterpret_cast<const float4*>(xa + kb) : z;
+      rb = bnv ? __ldg(reinterpret_cast<const float4*>(wb + kb)) : z;
     } else {
-#pragma unroll
-      for (int e = 0; e < 8; e++) {
-        const int k = kb + e;
-        ra[e] = (am && k < K) ? xa[k] : 0.0f;
-        rb[e] = (bnv && k < K) ? __ldg(wb + k) : 0.0f;
-      }
+      ra.x = (am && kb < K) ? xa[kb] : 0.f;
+      ra.y = (am && kb + 1 < K) ? xa[kb + 1] : 0.f;
+      ra.z = (am && kb + 2 < K) ? xa[kb + 2] : 0.f;
+      ra.w = (am && kb + 3 < K) ? xa[kb + 3] : 0.f;
+      rb.x = (bnv && kb < K) ? __ldg(wb + kb) : 0.f;
+      rb.y = (bnv && kb + 1 < K) ? __ldg(wb + kb + 1) : 0.f;
+      rb.z = (bnv && kb + 2 < K) ? __ldg(wb + kb + 2) : 0.f;
+      rb.w = (bnv && kb + 3 < K) ? __ldg(wb + kb + 3) : 0.f;
     }
   };
   auto store = [&](int b) {
-#pragma unroll
-    for (int e = 0; e < 8; e++) {
-      As[b][lk + e][lr] = ra[e];
-      Bs[b][lk + e][lr] = rb[e];
-    }
+    As[b][lk + 0][lr] = ra.x; As[b][lk + 1][lr] = ra.y;
+    As[b][lk + 2][lr] = ra.z; As[b][lk + 3][lr] = ra.w;
+    Bs[b][lk + 0][lr] = rb.x; Bs[b][lk + 1][lr] = rb.y;
+    Bs[b][lk + 2][lr] = rb.z; Bs[b][lk + 3][lr] = rb.w;
   };
   float acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; i++)
 #pragma unroll
     for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
+  // fragments double-buffered in registers: those of k+1 load while k multiplies
+  float4 fa[2][2], fb[2][2];
+  auto frag = [&](int b, int kk, int f) {
+    fa[f][0] = *reinterpret_cast<const float4*>(&As[b][kk][ty * 4]);
+    fa[f][1] = *reinterpret_cast<const float4*>(&As[b][kk][64 + ty * 4]);
+    fb[f][0] = *reinterpret_cast<const float4*>(&Bs[b][kk][tx * 4]);
+    fb[f][1] = *reinterpret_cast<const float4*>(&Bs[b][kk][64 + tx * 4]);
+  };
   load(0);
   store(0);
   __syncthreads();
-  const int nk = (K + BK - 1) / BK;
+  frag(0, 0, 0);
+  const int nk = (K + KB - 1) / KB;
   for (int kt = 0; kt < nk; kt++) {
     const int b = kt & 1;
-    if (kt + 1 < nk) load((kt + 1) * BK);
+    if (kt + 1 < nk) load((kt + 1) * KB);
 #pragma unroll
-    for (int kk = 0; kk < BK; kk++) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[b][kk][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[b][kk][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[b][kk][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[b][kk][64 + tx * 4]);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    for (int kk = 0; kk < KB; kk++) {
+      const int f = kk & 1;
+      if (kk + 1 < KB) frag(b, kk + 1, f ^ 1);
+      const float av[8] = {fa[f][0].x, fa[f][0].y, fa[f][0].z, fa[f][0].w,
+                           fa[f][1].x, fa[f][1].y, fa[f][1].z, fa[f][1].w};
+      const float bv[8] = {fb[f][0].x, fb[f][0].y, fb[f][0].z, fb[f][0].w,
+                           fb[f][1].x, fb[f][1].y, fb[f][1].z, fb[f][1].w};
 #pragma unroll
       for (int i = 0; i < 8; i++)
 #pragma unroll
@@ -101,6 +106,7 @@ __global__ void __launch_bounds__(GT, 2)
     if (kt + 1 < nk) {
       store(b ^ 1);
       __syncthreads();
+      frag(b ^ 1, 0, 0);
     }
   }
 #pragma unroll
@@ -186,13 +192,24 @@ __global__ void __launch_bounds__(OT)
       if (cnt[i]) atomicAdd(&counts[i], (unsigned long long)cnt[i]);
 }
 
+// Rows of n_in floats (any stride) -> rows of `ld` floats, 16-byte aligned,
+// so the first layer's GEMM can use float4 loads (padding is never read).
+__global__ void k_pad_rows(const float* __restrict__ x, long long ldx, int M, int n_in,
+                           float* __restrict__ y, int ld) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)M * n_in;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long m = t / n_in;
+    const int k = (int)(t - m * n_in);
+    y[m * ld + k] = x[m * ldx + k];
+  }
+}
+
 static int ensure_act(dmlp_net* net, size_t rows, int ld) {
   if (net->act_rows >= rows && net->act_ld >= ld) return DMLP_OK;
-  cudaFree(net->d_act[0]);
-  cudaFree(net->d_act[1]);
-  net->d_act[0] = net->d_act[1] = nullptr;
+  for (int b = 0; b < 3; b++) cudaFree(net->d_act[b]);
+  net->d_act[0] = net->d_act[1] = net->d_act[2] = nullptr;
   net->act_rows = 0;
-  for (int b = 0; b < 2; b++)
+  for (int b = 0; b < 3; b++)
     if (int rc = cuda_check(cudaMalloc(&net->d_act[b], rows * ld * sizeof(float)), "cudaMalloc"))
       return rc;
   net->act_rows = rows;
@@ -206,7 +223,7 @@ static int run_eval(dmlp_net* net, const float* x, long long n, float* out, cons
   DeviceGuard dg(net->device);
   if (int rc = cuda_check(dg.err, "cudaSetDevice")) return rc;
   const int L = net->dev.L;
-  int maxld = 4;  // activation row stride = input pitch of the consuming layer
+  int maxld = net->hl[0].pitch;  // activation row stride = input pitch of the consuming layer
   for (int l = 1; l < L; l++) maxld = maxld > net->hl[l].pitch ? maxld : net->hl[l].pitch;
   const long long chunk = n < 16384 ? n : 16384;
   if (int rc = ensure_act(net, (size_t)chunk, maxld)) return rc;
@@ -223,6 +240,12 @@ static int run_eval(dmlp_net* net, const float* x, long long n, float* out, cons
     const int M = (int)((n - m0) < chunk ? (n - m0) : chunk);
     const float* in = x + m0 * net->sizes[0];
     long long ldin = net->sizes[0];
+    if (L > 1 && (ldin % 4 != 0 || (reinterpret_cast<uintptr_t>(in) & 15) != 0)) {
+      k_pad_rows<<<sms * 4, 256, 0, st>>>(in, ldin, M, net->sizes[0], net->d_act[2],
+                                          net->hl[0].pitch);
+      in = net->d_act[2];
+      ldin = net->hl[0].pitch;
+    }
     int b = 0;
     for (int l = 0; l < L - 1; l++) {
       const HostLayer& h = net->hl[l];
