@@ -166,6 +166,7 @@ __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, 
       constexpr int FB = RES ? 4 : 8;
 #pragma unroll
       for (int j4 = 0; j4 < CH; j4 += FB) {
+        if (j4 >= jn) break;  // no rows of this group left (warp-uniform: a warp is in one group)
         float4 w[FB];
 #pragma unroll
         for (int i = 0; i < FB; i++)
