@@ -561,8 +561,10 @@ __device__ __forceinline__ void poll_batch(const unsigned long long* base, const
     for (int u = 0; u < U; u++)
       if (off[u] >= 0 && (uint32_t)(v[u] >> 32) != seq) done = false;
     if (done) return;
-    if (round == 0) t0 = clock64();
-    else if (clock64() - t0 > kSpinTimeoutCycles) spin_fail(err);
+    if ((round & 63) == 0) {  // the hang guard, off the per-round path (C5 +1.5%)
+      if (round == 0) t0 = clock64();
+      else if (clock64() - t0 > kSpinTimeoutCycles) spin_fail(err);
+    }
     if (DMLP_POLL_BACKOFF_NS > 0) __nanosleep(DMLP_POLL_BACKOFF_NS);
 #pragma unroll
     for (int u = 0; u < U; u++)
@@ -646,8 +648,10 @@ __device__ __forceinline__ void gather_quads(const SrcSlots& sl, int nq, int gs,
         if ((uint32_t)(w0 >> 32) == seq && (uint32_t)(w1 >> 32) == seq &&
             (uint32_t)(w2 >> 32) == seq && (uint32_t)(w3 >> 32) == seq)
           break;
-        if (round == 0) t0 = clock64();
-        else if (clock64() - t0 > kSpinTimeoutCycles) spin_fail(err);
+        if ((round & 63) == 0) {  // the hang guard, off the per-round path
+          if (round == 0) t0 = clock64();
+          else if (clock64() - t0 > kSpinTimeoutCycles) spin_fail(err);
+        }
       }
       reinterpret_cast<float4*>(v)[u] =
           make_float4(__uint_as_float((uint32_t)w0), __uint_as_float((uint32_t)w1),

@@ -12,7 +12,7 @@ subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, cap
 cubin = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
 dis = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cubin)], capture_output=True,
                      text=True).stdout.splitlines()
-addr_line, inside, cur = {}, False, "?"
+addr_line, inside, cur, chain = {}, False, "?", []
 for ln in dis:
     if ln.startswith(".text."):
         inside = kname in ln
@@ -21,9 +21,13 @@ for ln in dis:
         continue
     m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
     if m:
-        cur = os.path.basename(m.group(1)) + ":" + m.group(2)
+        chain.append(os.path.basename(m.group(1)) + ":" + m.group(2))
+        continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
     if m:
+        if chain:  # innermost first, the kernel-level line last
+            cur = chain[0] + (" @ " + chain[-1] if len(chain) > 1 else "")
+            chain = []
         addr_line[int(m.group(1), 16)] = cur
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
