@@ -39,16 +39,20 @@ __device__ __forceinline__ float tanh_scaled_noinline(float a, float* t) {
   return dev_scaled_tanh(a, t);
 }
 
-// Four consecutive flag words (16-byte aligned), the first `valid` of them.
+// Four consecutive flag words (32-byte aligned), the first `valid` of them.
+// A full quad is ONE 256-bit store (STG.E.ENL2.256): the 32-byte sector is
+// written whole instead of as two 16-byte halves from two instructions -- a
+// 2500-word backward exchange drops from 5.4K to 3.5K cycles
+// (scripts/mb/xchg11_mb.cu).  Each 8-byte element is still a single-copy-
+// atomic word carrying its own flag (vector accesses are per-element).
 __device__ __forceinline__ void st_flag4(unsigned long long* p, float4 x, int valid,
                                          uint32_t seq) {
   const unsigned long long h = (unsigned long long)seq << 32;
   const unsigned long long a = h | __float_as_uint(x.x), b = h | __float_as_uint(x.y);
   const unsigned long long c = h | __float_as_uint(x.z), d = h | __float_as_uint(x.w);
   if (valid >= 4) {
-    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b)
-                 : "memory");
-    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p + 2), "l"(c), "l"(d)
+    asm volatile("st.relaxed.gpu.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a),
+                 "l"(b), "l"(c), "l"(d)
                  : "memory");
   } else {
     if (valid > 0) st_flag(p, x.x, seq);

@@ -11,7 +11,19 @@
 using namespace dmlp;
 namespace cg = cooperative_groups;
 
-template <bool PAIR>
+__device__ __forceinline__ void st_flag4_256(unsigned long long* p, float4 x, int valid,
+                                             uint32_t seq) {
+  const unsigned long long h = (unsigned long long)seq << 32;
+  if (valid >= 4)
+    asm volatile("st.relaxed.gpu.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "l"(h | __float_as_uint(x.x)), "l"(h | __float_as_uint(x.y)),
+                 "l"(h | __float_as_uint(x.z)), "l"(h | __float_as_uint(x.w))
+                 : "memory");
+  else
+    st_flag4(p, x, valid, seq);
+}
+
+template <bool PAIR, bool V256 = false>
 __global__ void __launch_bounds__(512, 1) k_x(int F, int nr, unsigned long long* buf, int iters,
                                                long long* out, int* err) {
   __shared__ float red[512];
@@ -31,7 +43,8 @@ __global__ void __launch_bounds__(512, 1) k_x(int F, int nr, unsigned long long*
     if (!PAIR) {
       for (int q = tid; 4 * q < F; q += blockDim.x) {
         const float4 p = make_float4(c + 1.f, c + 2.f, c + 3.f, c + 4.f);
-        st_flag4(b + (size_t)c * stride + 4 * q, p, F - 4 * q, seq);
+        if (V256) st_flag4_256(b + (size_t)c * stride + 4 * q, p, F - 4 * q, seq);
+        else st_flag4(b + (size_t)c * stride + 4 * q, p, F - 4 * q, seq);
       }
     } else {
       const int lo = rank ? half : 0, hi = rank ? F : half;         // my columns
@@ -54,7 +67,7 @@ __global__ void __launch_bounds__(512, 1) k_x(int F, int nr, unsigned long long*
   if (res[0] == 12345.f) out[0] = 0;
 }
 
-template <bool PAIR>
+template <bool PAIR, bool V256 = false>
 void run(int F, int nr) {
   int* err; long long* d; unsigned long long* buf;
   cudaMalloc(&err, 4); cudaMalloc(&d, 148 * 8); cudaMalloc(&buf, 1 << 26);
@@ -65,17 +78,17 @@ void run(int F, int nr) {
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = PAIR ? 2 : 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at; cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_x<PAIR>, F, nr, buf, 2000, d, err);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_x<PAIR, V256>, F, nr, buf, 2000, d, err);
   cudaError_t e2 = cudaDeviceSynchronize();
   long long h[148]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   long long mx = 0; for (int i = 0; i < 148; i++) mx = h[i] > mx ? h[i] : mx;
-  printf("%s F=%4d nr=%2d cycles/exchange=%lld %s %s\n", PAIR ? "pair" : "flat", F, nr, mx,
+  printf("%s%s F=%4d nr=%2d cycles/exchange=%lld %s %s\n", PAIR ? "pair" : "flat", V256 ? "-256b" : "", F, nr, mx,
          cudaGetErrorString(e), cudaGetErrorString(e2));
   cudaFree(err); cudaFree(d); cudaFree(buf);
 }
 int main() {
   const int Fs[] = {1000, 1500, 2000, 2500}, nrs[] = {7, 11, 14, 17};
   for (int rep = 0; rep < 2; rep++)
-    for (int i = 0; i < 4; i++) { run<false>(Fs[i], nrs[i]); run<true>(Fs[i], nrs[i]); }
+    for (int i = 0; i < 4; i++) { run<false>(Fs[i], nrs[i]); run<false, true>(Fs[i], nrs[i]); }
   return 0;
 }
