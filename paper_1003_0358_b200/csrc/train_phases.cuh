@@ -638,17 +638,15 @@ __device__ __forceinline__ void gather_quads(const SrcSlots& sl, int nq, int gs,
     if (u >= nq) return;
     if ((sl.flat || (sl.R & 3) == 0) && 4 * u + 4 <= sl.fi) {
       // flat words, or producer blocks of a multiple of 4 rows: the quad is
-      // 4 consecutive, 32-byte aligned words -> two vector polls
+      // 4 consecutive, 32-byte aligned words -> one 256-bit vector poll
       const int p = 4 * u / sl.R;
       const unsigned long long* a =
           sl.src + (sl.flat ? 4 * u : (p << sl.ylog) + (4 * u - p * sl.R));
       unsigned long long w0, w1, w2, w3;
       long long t0 = 0;
       for (int round = 0;; round++) {
-        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
-                     : "=l"(w0), "=l"(w1) : "l"(a) : "memory");
-        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
-                     : "=l"(w2), "=l"(w3) : "l"(a + 2) : "memory");
+        asm volatile("ld.relaxed.gpu.global.v4.b64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(a) : "memory");
         if ((uint32_t)(w0 >> 32) == seq && (uint32_t)(w1 >> 32) == seq &&
             (uint32_t)(w2 >> 32) == seq && (uint32_t)(w3 >> 32) == seq)
           break;
