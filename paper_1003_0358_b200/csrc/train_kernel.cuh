@@ -276,11 +276,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- output layer: partials of the owned columns ----------------
     const float* yin = H > 0 ? sm + net.yown_off : in0;
     __syncthreads();
-    if (oown && tid < lo.fo) {
-      const float* wr = otile + tid * OT;
+    // fo partials, padded with zero words up to whole 32-byte sectors (the
+    // slot is line aligned): no partially written sector
+    if (oown && tid < ((lo.fo + 3) & ~3)) {
       float a = 0.0f;
-      for (int k = 0; k < onc; k++) a = fmaf(wr[k], yin[k], a);
-      if (c == 0) a += wr[OT - 1];  // bias
+      if (tid < lo.fo) {
+        const float* wr = otile + tid * OT;
+        for (int k = 0; k < onc; k++) a = fmaf(wr[k], yin[k], a);
+        if (c == 0) a += wr[OT - 1];  // bias
+      }
       st_flag(lo.yll + ((size_t)buf * lo.P << lo.ylog) + ((size_t)c << lo.ylog) + tid, a, seq);
     }
     PH(5);
