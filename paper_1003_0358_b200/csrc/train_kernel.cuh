@@ -357,9 +357,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < NRL; i++)
             if (net.reg_layer[i] == l)
               reg_partials<RR, RC, RS>(wr[i], sm + ly.wsm_off, ly.fi, g_nr[l], dl, ps, seq);
-        } else if ((FEAT & kFeatSmem) && ly.res == kResSmem)
-          bwd_partials<true, false>(reinterpret_cast<float4*>(sm + ly.wsm_off), ly.pitch >> 2,
-                                    ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
+        } else if ((FEAT & kFeatSmem) && ly.res == kResSmem) {
+          // plans without register rows, <= 8 rows per thread group: the
+          // update is fused into the same pass (every row's weights in flight,
+          // the partials published before the updated weights are stored: one
+          // read, one write per weight; C2 +2%).  Elsewhere it measured slower
+          // (C4 -2 to -5%, C3 -3%): those layers update separately while the
+          // partials travel
+          if (NRL == 0 && (((g_nr[l] - 1) >> ly.gs) + 1) <= 8)
+            bwd_partials<true, true>(reinterpret_cast<float4*>(sm + ly.wsm_off), ly.pitch >> 2,
+                                     ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
+          else
+            bwd_partials<true, false>(reinterpret_cast<float4*>(sm + ly.wsm_off), ly.pitch >> 2,
+                                      ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
+        }
         else if (FEAT & kFeatL2)
           bwd_partials<false, true>(
               reinterpret_cast<float4*>(ly.w + (size_t)g_r0[l] * ly.pitch), ly.pitch >> 2,
@@ -367,7 +378,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       PHL(8, l, 2);
       TRACE(1 + 2 * (L - 1 + (H - 1 - l)));
-      if ((FEAT & kFeatSmem) && mine && ly.res == kResSmem)
+      if ((FEAT & kFeatSmem) && mine && ly.res == kResSmem &&
+          !(NRL == 0 && (((g_nr[l] - 1) >> ly.gs) + 1) <= 8))
         update_rows<true>(reinterpret_cast<float4*>(sm + ly.wsm_off), ly.pitch >> 2, ly.gs,
                           g_nr[l], reinterpret_cast<const float4*>(sm + ly.in_off), sl);
       if (mine && ly.res == kResReg) {
