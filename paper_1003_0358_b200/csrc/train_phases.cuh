@@ -327,94 +327,6 @@ __device__ __forceinline__ void update_rows(float4* W4, int nq, int gs, int nr,
   }
 }
 
-// ---- layer-0 look-ahead ------------------------------------
-// The first hidden layer's input x(s+1) is known a sample ahead, so its
-// forward leaves the per-sample dependency chain: while sample s runs, the
-// CTA applies the PENDING update of its layer-0 rows (sample s-1's
-// eta*delta, x(s-1): w + (eta*delta_k)*x_i, mul then add as kernels.py:174)
-// and forms p_k = W0(s-1)[k] . x(s+1); sample s+1 then only adds its own
-// pending rank-1 term, a0 = p_k + (eta*delta_k(s)) * (x(s) . x(s+1)), and
-// applies the tanh.  The stored layer-0 rows are therefore always one update
-// behind; the launch epilogue leaves that update pending in global memory
-// (NetDev::l0_pend_*) for the next launch or for the readers, which apply it
-// (dmlp_net_get_layer, evaluation, dmlp_net_flush).
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Rows [0, nr) of the CTA's layer-0 block (nq float4 quads per row): warp w
-// takes rows w, w+16, ... two at a time, its lanes the quads lane, lane+32,
-// ... (QB of them in flight per row).  upd: apply the pending update first
-// (the stored rows become W0(s-1)); xnext (may be null): p[k] = row . xnext,
-// lane partials in quad order, then a fixed butterfly.
-template <bool RES>
-__device__ __forceinline__ void l0_pass(float4* W4, int nq, int nr, bool upd,
-                                        const float* __restrict__ dsc,
-                                        const float4* __restrict__ xprev,
-                                        const float4* __restrict__ xnext, float* p) {
-  constexpr int QB = 4;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k0 = warp; k0 < nr; k0 += 2 * kWarps) {
-    const int k1 = k0 + kWarps;
-    const bool two = k1 < nr;
-    const float d0 = upd ? dsc[k0] : 0.0f, d1 = (upd && two) ? dsc[k1] : 0.0f;
-    float4* r0 = W4 + (size_t)k0 * nq;
-    float4* r1 = W4 + (size_t)(two ? k1 : k0) * nq;
-    float a0 = 0.0f, a1 = 0.0f;
-    for (int qb = lane; qb < nq; qb += 32 * QB) {
-      float4 w0[QB], w1[QB];
-#pragma unroll
-      for (int b = 0; b < QB; b++) {
-        const int q = qb + 32 * b;
-        if (q < nq) {
-          w0[b] = ldw4<RES>(r0 + q);
-          if (two) w1[b] = ldw4<RES>(r1 + q);
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < QB; b++) {
-        const int q = qb + 32 * b;
-        if (q >= nq) continue;
-        if (upd) {
-          const float4 xp = xprev[q];
-          w0[b] = upd4(w0[b], d0, xp);
-          stw4<RES>(r0 + q, w0[b]);
-          if (two) {
-            w1[b] = upd4(w1[b], d1, xp);
-            stw4<RES>(r1 + q, w1[b]);
-          }
-        }
-        if (xnext) {
-          const float4 xn = xnext[q];
-          a0 = dot4(w0[b], xn, a0);
-          if (two) a1 = dot4(w1[b], xn, a1);
-        }
-      }
-    }
-    if (xnext) {
-      a0 = warp_sum(a0);
-      a1 = warp_sum(a1);
-      if (lane == 0) {
-        p[k0] = a0;
-        if (two) p[k1] = a1;
-      }
-    }
-  }
-}
-
-// a . b over nq float4 quads by one warp (lane partials in quad order, then a
-// fixed butterfly); every lane returns the sum.
-__device__ __forceinline__ float warp_dot4(const float4* __restrict__ a,
-                                           const float4* __restrict__ b, int nq) {
-  const int lane = threadIdx.x & 31;
-  float s = 0.0f;
-  for (int q = lane; q < nq; q += 32) s = dot4(a[q], b[q], s);
-  return warp_sum(s);
-}
-
 // ---- register-resident row blocks -------------------------------------------
 // A hidden layer whose owned rows do not fit in shared memory can live in the
 // register file (256 KB per SM): thread t holds column t + 512*m (m < RC) of
