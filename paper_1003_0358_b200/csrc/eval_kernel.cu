@@ -31,6 +31,26 @@ constexpr int BM = 128, BN = 128, BK = 16, GT = 256;
 // a 3-stage pipeline of transposing 4-byte cp.async measured 27.8, and one
 // CTA per SM with more registers 34.6).  Thread (ty, tx) owns rows
 // ty*4 + {0..3, 64..67} and columns tx*4 + {0..3, 64..67}.
+// Packed fp32 pairs for FFMA2 (fma.rn.f32x2: two independent round-to-nearest
+// FMAs per instruction -- the same results as two fmaf).  On sm_100 a scalar
+// FFMA issues at most every other cycle per SMSP, so the fp32 SIMT peak needs
+// the packed form; the broadcast operand (a, a) becomes a scalar .F32
+// operand in SASS, no extra moves.
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void fma2(unsigned long long& acc, unsigned long long a,
+                                     unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float2 unpack2(unsigned long long v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return make_float2(a, b);
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(GT, 2)
     k_gemm_tanh(const float* __restrict__ X, long long ldx, const float* __restrict__ W, int ldw,
@@ -69,11 +89,11 @@ __global__ void __launch_bounds__(GT, 2)
     Bs[b][lk + 0][lr] = rb.x; Bs[b][lk + 1][lr] = rb.y;
     Bs[b][lk + 2][lr] = rb.z; Bs[b][lk + 3][lr] = rb.w;
   };
-  float acc[8][8];
+  unsigned long long acc[8][4];  // (acc[i][2p], acc[i][2p+1]) packed for FFMA2
 #pragma unroll
   for (int i = 0; i < 8; i++)
 #pragma unroll
-    for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
+    for (int j = 0; j < 4; j++) acc[i][j] = 0ull;
   // fragments double-buffered in registers: those of k+1 load while k multiplies
   float4 fa[2][2], fb[2][2];
   auto frag = [&](int b, int kk, int f) {
@@ -96,12 +116,14 @@ __global__ void __launch_bounds__(GT, 2)
       if (kk + 1 < KB) frag(b, kk + 1, f ^ 1);
       const float av[8] = {fa[f][0].x, fa[f][0].y, fa[f][0].z, fa[f][0].w,
                            fa[f][1].x, fa[f][1].y, fa[f][1].z, fa[f][1].w};
-      const float bv[8] = {fb[f][0].x, fb[f][0].y, fb[f][0].z, fb[f][0].w,
-                           fb[f][1].x, fb[f][1].y, fb[f][1].z, fb[f][1].w};
+      const unsigned long long bp[4] = {pack2(fb[f][0].x, fb[f][0].y), pack2(fb[f][0].z, fb[f][0].w),
+                                        pack2(fb[f][1].x, fb[f][1].y), pack2(fb[f][1].z, fb[f][1].w)};
 #pragma unroll
-      for (int i = 0; i < 8; i++)
+      for (int i = 0; i < 8; i++) {
+        const unsigned long long aa = pack2(av[i], av[i]);
 #pragma unroll
-        for (int j = 0; j < 8; j++) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; j++) fma2(acc[i][j], aa, bp[j]);
+      }
     }
     if (kt + 1 < nk) {
       store(b ^ 1);
@@ -117,7 +139,8 @@ __global__ void __launch_bounds__(GT, 2)
     for (int j = 0; j < 8; j++) {
       const int n = bn + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
       if (n >= N) continue;
-      const float a = acc[i][j] + __ldg(W + (long long)n * ldw + K);
+      const float2 pr = unpack2(acc[i][j >> 1]);
+      const float a = ((j & 1) ? pr.y : pr.x) + __ldg(W + (long long)n * ldw + K);
       float t;
       Y[(long long)m * ldy + n] = dev_scaled_tanh(a, &t);
     }
