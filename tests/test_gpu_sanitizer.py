@@ -55,3 +55,16 @@ def test_train_kernel_sanitizer(tmp_path, tool, feat, sizes):
     out = p.stdout + p.stderr
     assert p.returncode == 0 and "ok " in out, out[-3000:]
     assert "ERROR SUMMARY: 0 errors" in out or "0 hazards" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_deform_eval_sanitizer(tool):
+    """memcheck / racecheck of the deformation (4 images per CTA, ragged last
+    batch, unaligned raw rows, another kernel size), upscale and evaluation
+    (padded-input GEMM path) kernels: scripts/memcheck_deform_eval.py."""
+    p = subprocess.run([_sanitizer(), "--tool", tool, "--print-limit", "4", "--error-exitcode", "9",
+                        sys.executable, os.path.join(ROOT, "scripts", "memcheck_deform_eval.py")],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0 and "ok " in out, out[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "0 hazards" in out, out[-3000:]
