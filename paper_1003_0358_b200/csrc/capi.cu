@@ -52,7 +52,7 @@ int net_end(dmlp_net* net, cudaStream_t st) {
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 // Plan-override knobs for A/B experiments (DMLP_YFLAT, DMLP_GS,
-// DMLP_FORCE_VARIANT, DMLP_FEAT).  Read only in builds made with
+// DMLP_FORCE_VARIANT, DMLP_FEAT, DMLP_SMEM_EXCLUDE).  Read only in builds made with
 // -DDMLP_EXPERIMENT_KNOBS (scripts/ab_perf.sh); the product library never
 // lets the environment change a net's kernel plan.
 static const char* knob(const char* name) {
@@ -261,8 +261,10 @@ static double auto_plan(dmlp_net* net, bool noreg, int smem_cap, unsigned all) {
       regf += pf;
     }
     if (tv.n_reg > 0 && regmask == 0) continue;
+    unsigned excl = 0;  // experiments: hidden layers kept out of shared memory
+    if (const char* ex = knob("DMLP_SMEM_EXCLUDE")) excl = (unsigned)atoi(ex);
     for (unsigned m = 0; m <= all; m++) {
-      if (m & regmask) continue;
+      if (m & (regmask | excl)) continue;
       if (layout_smem(net, m, regmask, tv.rr * tv.rs * kThreads) > smem_cap) continue;
       const long long f = resident_floats(d, m) + regf;
       // ties go to the simpler plan, except that a plan holding every hidden
