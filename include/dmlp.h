@@ -183,6 +183,14 @@ int dmlp_gradient_check(const int32_t *sizes, int32_t n_sizes, const double *w_h
 int dmlp_tanhf_check(uint64_t *mismatches, uint32_t *first_bad);
 int dmlp_tanhf_eval(const float *x_dev, float *y_dev, int64_t n);
 
+/* The training kernel's faithfully rounded tanhf (dev_tanhf_fast) over all
+ * non-NaN floats: stats[0] inputs where it differs from the glibc
+ * restatement, stats[1] the largest difference in ulp; stats[2], stats[3]
+ * the same against the correctly rounded tanh.  And evaluation on given
+ * inputs (device pointers). */
+int dmlp_tanhf_fast_check(uint64_t *stats);
+int dmlp_tanhf_fast_eval(const float *x_dev, float *y_dev, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

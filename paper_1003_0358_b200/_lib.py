@@ -60,6 +60,8 @@ SIGNATURES = [
     ("dmlp_tanhf_check", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64),
                                         ctypes.POINTER(ctypes.c_uint32)]),
     ("dmlp_tanhf_eval", ctypes.c_int, [P, P, i64]),
+    ("dmlp_tanhf_fast_check", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64)]),
+    ("dmlp_tanhf_fast_eval", ctypes.c_int, [P, P, i64]),
     ("dmlp_gradient_check", ctypes.c_int, [I32P, i32, P, P, i32, ctypes.c_double, P, P,
                                            ctypes.POINTER(ctypes.c_double)]),
 ]

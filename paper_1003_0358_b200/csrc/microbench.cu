@@ -328,6 +328,35 @@ __global__ void k_tanhf_check(unsigned long long start, unsigned long long count
     }
   }
 }
+// The training kernel's dev_tanhf_fast over every non-NaN float: st[0] inputs
+// where it differs from the glibc restatement, st[1] the largest difference
+// in ulp; st[2], st[3] the same against the correctly rounded tanh (CUDA's
+// double tanh, rounded to float).
+__global__ void k_tanhf_fast_check(unsigned long long* st) {
+  unsigned long long dg = 0, dc = 0, mg = 0, mc = 0;
+  for (unsigned long long u = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       u < (1ull << 32); u += (unsigned long long)gridDim.x * blockDim.x) {
+    const float x = u2f((uint32_t)u);
+    if (x != x) continue;
+    const long long a = (int32_t)f2u(dev_tanhf_fast(x)), g = (int32_t)f2u(dev_tanhf(x));
+    const long long c = (int32_t)f2u(__double2float_rn(tanh((double)x)));
+    const unsigned long long eg = (unsigned long long)(a > g ? a - g : g - a);
+    const unsigned long long ec = (unsigned long long)(a > c ? a - c : c - a);
+    dg += eg != 0;
+    dc += ec != 0;
+    mg = eg > mg ? eg : mg;
+    mc = ec > mc ? ec : mc;
+  }
+  atomicAdd(st + 0, dg);
+  atomicMax(st + 1, mg);
+  atomicAdd(st + 2, dc);
+  atomicMax(st + 3, mc);
+}
+__global__ void k_tanhf_fast_eval(const float* x, float* y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = dev_tanhf_fast(x[i]);
+}
 __global__ void k_tanhf_eval(const float* x, float* y, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -353,6 +382,23 @@ int dmlp_tanhf_check(uint64_t* mismatches, uint32_t* first_bad) {
   cudaFree(d);
   cudaFree(f);
   return DMLP_OK;
+}
+
+int dmlp_tanhf_fast_check(uint64_t* stats) {
+  unsigned long long* d = nullptr;
+  if (int rc = cuda_check(cudaMalloc(&d, 32), "cudaMalloc")) return rc;
+  cudaMemset(d, 0, 32);
+  dmlp::k_tanhf_fast_check<<<148 * 8, 256>>>(d);
+  int rc = cuda_check(cudaGetLastError(), "k_tanhf_fast_check");
+  if (!rc) rc = cuda_check(cudaMemcpy(stats, d, 32, cudaMemcpyDeviceToHost), "cudaMemcpy");
+  cudaFree(d);
+  return rc;
+}
+
+int dmlp_tanhf_fast_eval(const float* x_dev, float* y_dev, int64_t n) {
+  if (n <= 0) return DMLP_OK;
+  dmlp::k_tanhf_fast_eval<<<148 * 4, 256>>>(x_dev, y_dev, n);
+  return cuda_check(cudaGetLastError(), "k_tanhf_fast_eval");
 }
 
 int dmlp_tanhf_eval(const float* x_dev, float* y_dev, int64_t n) {

@@ -82,6 +82,8 @@ def test_train_epoch_1000_steps_headline(golden, cfg):
     tag = f"{cfg} plan {dn.layer_residency} ({dn.n_ctas} CTAs) after {n} steps;"
     p = pred.cpu().numpy().astype(np.int64)
     bad = np.nonzero(p != np.array(pref))[0]
+    print(f"\nDRIFT {cfg} max|dW|/max|W| " + " ".join(f"{m:.2e}" for m, _ in dr) +
+          " | ||dW||/||W|| " + " ".join(f"{nm:.2e}" for _, nm in dr))
     assert len(bad) == 0, (f"{tag} argmax differs at samples {bad[:10].tolist()}; "
                            f"drift {[f'{m:.1e}' for m, _ in dr]}")
     assert int(wrong.item()) == wrong_ref, tag

@@ -182,6 +182,47 @@ def test_device_tanhf_matches_libm():
     assert same.all(), x[~same][:5]
 
 
+def test_device_tanhf_fast_exhaustive():
+    """The training kernel's tanhf (dev_tanhf_fast) on every non-NaN float:
+    faithfully rounded (within 1 ulp of the correctly rounded tanh), within
+    2 ulp of glibc's tanhf (itself within 2 ulp of correctly rounded), and
+    equal to glibc's on more than 97% of inputs."""
+    import ctypes
+
+    from paper_1003_0358_b200 import _lib
+
+    st = (ctypes.c_uint64 * 4)()
+    _lib.check(_lib.lib().dmlp_tanhf_fast_check(st), "dmlp_tanhf_fast_check")
+    differ_glibc, ulp_glibc, differ_cr, ulp_cr = list(st)
+    assert ulp_cr <= 1 and ulp_glibc <= 2, list(st)
+    assert differ_glibc < 0.03 * 2**32, list(st)
+
+
+def test_device_tanhf_fast_edges():
+    """Edge values of the kernel's tanhf: signed zeros, infinities, NaN,
+    subnormals, the branch point 0.55 and the saturation region, against the
+    host glibc tanhf within 2 ulp (signs and specials exact)."""
+    import torch
+
+    from paper_1003_0358_b200 import _lib
+
+    x = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45, 1e-38, 1e-30, 1e-8,
+                  0.5499999, 0.55, 0.5500001, -0.55, 1.0, 9.0, 9.1, 10.0, 10.5, 20.0, 88.0,
+                  -88.0, 1e30, -1e30], np.float32)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    _lib.check(_lib.lib().dmlp_tanhf_fast_eval(xd.data_ptr(), yd.data_ptr(), x.size),
+               "tanhf_fast_eval")
+    y = yd.cpu().numpy()
+    L = O.lib()
+    ref = np.array([L.or_tanhf(float(v)) for v in x], np.float32)
+    nan = np.isnan(ref)
+    assert np.isnan(y[nan]).all()
+    assert (np.signbit(y[~nan]) == np.signbit(ref[~nan])).all()
+    ulp = np.abs(y[~nan].view(np.int32).astype(np.int64) - ref[~nan].view(np.int32))
+    assert ulp.max() <= 2, list(zip(x[~nan], y[~nan], ref[~nan]))
+
+
 @pytest.mark.parametrize("sizes,n_ctas", [
     ((841, 10), 0),                      # no hidden layer: one CTA, output tile = all inputs
     ((841, 5000, 10), 0),                # 34 rows per CTA: two reduction chunks, > 32-row gathers
