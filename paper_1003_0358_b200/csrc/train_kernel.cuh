@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (k < onc) {
           const float yk = yin[k];
           float acc = 0.0f;
+#pragma unroll 10
           for (int j = 0; j < lo.fo; j++) {
             const float w = otile[j * OT + k];
             acc = __fadd_rn(acc, __fmul_rn(w, dout[j]));
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm[net.dsc_off[0] + k] = __fmul_rn(eta, d);
           }
         } else {  // bias column (CTA 0): w + (eta*delta)*1
+#pragma unroll 10
           for (int j = 0; j < lo.fo; j++)
             otile[j * OT + OT - 1] = __fadd_rn(otile[j * OT + OT - 1], sout[j]);
         }
