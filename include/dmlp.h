@@ -95,6 +95,10 @@ int dmlp_net_read_profile(dmlp_net *net, int64_t *slots);
  * k = 0 forward, 1 gather of its input, 2 column partials, 3 update,
  * 4 gather of the partials by the layer below.  Fills n_slots (<= 96). */
 int dmlp_net_read_profile_all(dmlp_net *net, int64_t *slots, int32_t n_slots);
+/* The same per CTA, unsummed: slots[c * 96 + k] (96 words per CTA: the 16
+ * phase slots -- slot 12 = the CTA's SM id + 1, per launch -- then 5 per
+ * layer), and reset. */
+int dmlp_net_read_profile_cta(dmlp_net *net, int64_t *slots);
 /* One-sample timeline of the next launches: every CTA records %globaltimer
  * at 64 marks of sample `sample` (mark 0 start; for exchange e, 1+2e = its
  * contribution published, 2+2e = its gather done; 63 end).  marks (optional,

@@ -44,6 +44,7 @@ SIGNATURES = [
     ("dmlp_net_profile", ctypes.c_int, [P, i32]),
     ("dmlp_net_read_profile", ctypes.c_int, [P, I64P]),
     ("dmlp_net_read_profile_all", ctypes.c_int, [P, I64P, i32]),
+    ("dmlp_net_read_profile_cta", ctypes.c_int, [P, P]),
     ("dmlp_net_trace", ctypes.c_int, [P, i64, P]),
     ("dmlp_net_set_layer", ctypes.c_int, [P, i32, P, i64]),
     ("dmlp_net_get_layer", ctypes.c_int, [P, i32, P, i64]),

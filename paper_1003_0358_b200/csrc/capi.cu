@@ -608,6 +608,19 @@ int dmlp_net_read_profile_all(dmlp_net* net, int64_t* slots, int32_t n_slots) {
   return DMLP_OK;
 }
 
+int dmlp_net_read_profile_cta(dmlp_net* net, int64_t* slots) {
+  if (!net || !slots) return set_error(DMLP_EINVAL, "null argument");
+  if (!net->dev.prof) return set_error(DMLP_EINVAL, "profiling is not enabled");
+  DeviceGuard dg(net->device);
+  DMLP_CUDA(dg.err);
+  DMLP_CUDA(cudaDeviceSynchronize());
+  const int n = kProfWords * net->dev.nct;
+  DMLP_CUDA(cudaMemcpy(slots, net->dev.prof, n * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost));
+  DMLP_CUDA(cudaMemset(net->dev.prof, 0, n * sizeof(unsigned long long)));
+  return DMLP_OK;
+}
+
 int dmlp_net_read_profile(dmlp_net* net, int64_t* slots) {
   return dmlp_net_read_profile_all(net, slots, kProfPhases);
 }

@@ -68,7 +68,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(16) float sm[];
   __shared__ int g_r0[kMaxLayers], g_nr[kMaxLayers];
   __shared__ int g_rb[kMaxLayers];  // forward reduction buffer offset per layer
-  const int c = blockIdx.x, tid = threadIdx.x;
+#ifndef DMLP_CTA_ROT
+#define DMLP_CTA_ROT 0  // experiments: logical CTA = (blockIdx + ROT) mod grid
+#endif
+  const int c = DMLP_CTA_ROT ? (blockIdx.x + DMLP_CTA_ROT) % gridDim.x : blockIdx.x;
+  const int tid = threadIdx.x;
   const int L = net.L, H = L - 1;  // H hidden layers
   float* red = sm + net.red_off;
   float* pbuf = sm + net.pbuf_off;
@@ -154,6 +158,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // thread 0's clocks live in smem: no registers held across the loop
   __shared__ long long pt[4];  // loop start, exchange total, exchange mark, phase mark
   if (prof) pt[0] = pt[3] = clock64(), pt[1] = pt[2] = 0;
+  if (prof) {  // slot 12: the SM this CTA ran on, + 1 (per-CTA readout: dmlp_net_read_profile_cta)
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    ph[12] = smid + 1;
+  }
 #define t_loop0 pt[0]
 #define t_xchg pt[1]
 #define t_mark pt[2]

@@ -120,7 +120,7 @@ class DeviceNet:
         _lib.check(_lib.lib().dmlp_net_profile(self._h, int(bool(enable))), "dmlp_net_profile")
 
     PROFILE_SLOTS = ("loop", "exchange", "head", "fwd", "fwd_xchg", "out_part", "out_xchg",
-                     "out_stage", "bwd_part", "bwd_upd", "bwd_xchg", "upd0", "s12", "s13", "s14",
+                     "out_stage", "bwd_part", "bwd_upd", "bwd_xchg", "upd0", "smid", "s13", "s14",
                      "s15")
 
     LAYER_KINDS = ("fwd", "fwd_gather", "bwd_part", "bwd_upd", "bwd_gather")
@@ -133,12 +133,22 @@ class DeviceNet:
         buf = (ctypes.c_int64 * n)()
         _lib.check(_lib.lib().dmlp_net_read_profile_all(self._h, buf, n),
                    "dmlp_net_read_profile_all")
-        d = {k: buf[i] for i, k in enumerate(self.PROFILE_SLOTS)}
+        d = {k: buf[i] for i, k in enumerate(self.PROFILE_SLOTS) if k != "smid"}
         d["exchange_fraction"] = (d["exchange"] / d["loop"]) if d["loop"] else 0.0
         L = len(self.layer_sizes) - 1
         d["layers"] = [{k: buf[16 + 5 * l + j] for j, k in enumerate(self.LAYER_KINDS)}
                        for l in range(L)]
         return d
+
+    def read_profile_cta(self):
+        """Per-CTA profile since the last read: (sm, slots) -- the SM id each
+        CTA ran on (valid when one launch was profiled) and the raw
+        (n_ctas, 96) cycle slots (layout as read_profile)."""
+        buf = np.zeros((self.n_ctas, 96), dtype=np.int64)
+        _lib.check(_lib.lib().dmlp_net_read_profile_cta(self._h,
+                                                        buf.ctypes.data_as(ctypes.c_void_p)),
+                   "dmlp_net_read_profile_cta")
+        return buf[:, 12] - 1, buf
 
     def trace(self, sample: int = -1):
         """Arm a one-sample %globaltimer trace for the next launches (sample
