@@ -30,6 +30,7 @@ UNITS = {
     "train_inst_f0.cu": [],
     "train_inst_f1.cu": [],
     "train_inst_f3.cu": [],
+    "train_inst_f7.cu": [],
     "train_glue.cu": [],
     "eval_kernel.cu": [],
     "deform_kernel.cu": ["-fmad=false"],

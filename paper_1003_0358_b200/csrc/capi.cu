@@ -436,6 +436,18 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     int feat = 0;
     for (int l = 0; l < H; l++)
       feat |= d.ly[l].res == kResSmem ? kFeatSmem : d.ly[l].res == kResL2 ? kFeatL2 : 0;
+    // L1 for the one streamed layer l >= 1 (layer 0 resident, <= 8 rows per
+    // thread, its first kL1Rows rows per thread within kL1Budget)
+    int streamed = 0, l1ok = H > 0 && d.ly[0].res != kResL2;
+    for (int l = 1; l < H; l++) {
+      const LayerDev& ly = d.ly[l];
+      if (ly.res != kResL2) continue;
+      const int nj = (ly.R + (1 << ly.gs) - 1) >> ly.gs;
+      streamed++;
+      l1ok = l1ok && nj <= 8 && nj >= kL1Rows &&
+             kL1Rows * (1 << ly.gs) * ly.pitch * (int)sizeof(float) <= kL1Budget;
+    }
+    if (streamed == 1 && l1ok) feat |= kFeatL1;
     if (allpaths) feat = kFeatSmem | kFeatL2;  // sanitizer runs: every residency path
     net->train_fn = train_instance(vars[net->variant], feat);
     net->train_fn_prof = vars[net->variant].fn_prof;

@@ -132,10 +132,14 @@ cudaError_t launch_train(const dmlp_net* net, const float* x, long long ldx,
 // Compiled instantiations of the training kernel: n_reg register row blocks
 // of at most rr rows x rc columns per thread (0 = none), plus rs column
 // slots per thread in shared memory.
-enum { kFeatSmem = 1, kFeatL2 = 2 };  // residency paths compiled into an instance
+// residency paths compiled into an instance; kFeatL1: the streamed layer's
+// first kL1Rows rows per thread through L1 (train_phases.cuh: ldw4)
+enum { kFeatSmem = 1, kFeatL2 = 2, kFeatL1 = 4 };
+constexpr int kL1Rows = 5;            // 5 x 1504 floats: C4's layer 3, 30 KB of L1
+constexpr int kL1Budget = 30 * 1024;  // bytes per SM (the 228 KB carve-out leaves 28 KB)
 struct TrainVariant {
   int n_reg, rr, rc, rs;  // rs: column slots of each block kept in a shared-memory tail
-  const void* fn[4];      // by feature set (kFeatSmem | kFeatL2), no profile hooks; may be null
+  const void* fn[8];      // by feature set (kFeatSmem | kFeatL2 | kFeatL1), no profile hooks; may be null
   const void* fn_prof;    // every feature plus the profile / trace hooks
 };
 int train_variants(const TrainVariant** out);

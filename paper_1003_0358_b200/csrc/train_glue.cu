@@ -10,6 +10,7 @@ namespace dmlp {
 void train_fns_f0(const void** fns, const void** prof);
 void train_fns_f1(const void** fns, const void** prof);
 void train_fns_f3(const void** fns, const void** prof);
+void train_fns_f7(const void** fns, const void** prof);
 
 int train_variants(const TrainVariant** out) {
   static TrainVariant table[] = {
@@ -22,15 +23,18 @@ int train_variants(const TrainVariant** out) {
     const void* f0[n] = {};
     const void* f1[n] = {};
     const void* f3[n] = {};
+    const void* f7[n] = {};
     const void* pr[n] = {};
     train_fns_f0(f0, nullptr);
     train_fns_f1(f1, nullptr);
     train_fns_f3(f3, pr);
+    train_fns_f7(f7, nullptr);
     for (int k = 0; k < n; k++) {
       table[k].fn[0] = f0[k];
       table[k].fn[1] = f1[k];
       table[k].fn[2] = nullptr;  // L2 without shared memory: the full instance
       table[k].fn[3] = f3[k];
+      table[k].fn[7] = f7[k];  // + L1-cached streamed rows
       table[k].fn_prof = pr[k];
     }
     ready = true;
@@ -40,7 +44,7 @@ int train_variants(const TrainVariant** out) {
 }
 
 const void* train_instance(const TrainVariant& tv, int feat) {
-  for (int f = feat; f < 4; f++)  // the smallest compiled superset of the features
+  for (int f = feat; f < 8; f++)  // the smallest compiled superset of the features
     if ((f & feat) == feat && tv.fn[f]) return tv.fn[f];
   return tv.fn[3];
 }

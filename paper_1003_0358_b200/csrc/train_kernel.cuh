@@ -74,6 +74,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int c = DMLP_CTA_ROT ? (blockIdx.x + DMLP_CTA_ROT) % gridDim.x : blockIdx.x;
   const int tid = threadIdx.x;
   const int L = net.L, H = L - 1;  // H hidden layers
+  // streamed rows per thread cached in L1 (kFeatL1 instances: layer 0 is never
+  // streamed there, and the one streamed layer has <= 8 rows per thread)
+  constexpr int kL1R = (FEAT & kFeatL1) ? kL1Rows : 0;
   float* red = sm + net.red_off;
   float* pbuf = sm + net.pbuf_off;
   float* outv = sm + net.out_off;  // a | y | delta | eta*delta
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fwd_dispatch<true>(reinterpret_cast<const float4*>(sm + ly.wsm_off), ly, g_nr[l], v4,
                              redl, sm + ly.t_off, yo, ys, seq, (prof && l == 0) ? ph + 14 : nullptr);
         else if (FEAT & kFeatL2)
-          fwd_dispatch<false>(reinterpret_cast<const float4*>(ly.w + (size_t)g_r0[l] * ly.pitch),
+          fwd_dispatch<false, kL1R>(reinterpret_cast<const float4*>(ly.w + (size_t)g_r0[l] * ly.pitch),
                               ly, g_nr[l], v4, redl, sm + ly.t_off, yo, ys, seq);
       }
       PHL(3, l, 0);
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
         }
         else if (FEAT & kFeatL2)
-          bwd_partials<false, true>(
+          bwd_partials<false, true, kL1R>(
               reinterpret_cast<float4*>(ly.w + (size_t)g_r0[l] * ly.pitch), ly.pitch >> 2,
               ly.fi, ly.gs, g_nr[l], dl, sl, v4, pbuf, ps, seq);
       }
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         update_rows<true>(reinterpret_cast<float4*>(sm + l0.wsm_off), l0.pitch >> 2, l0.gs,
                           g_nr[0], x4, sm + net.dsc_off[cur]);
       else if (FEAT & kFeatL2)
-        update_rows<false>(reinterpret_cast<float4*>(l0.w + (size_t)g_r0[0] * l0.pitch),
+        update_rows<false, kL1R>(reinterpret_cast<float4*>(l0.w + (size_t)g_r0[0] * l0.pitch),
                            l0.pitch >> 2, l0.gs, g_nr[0], x4, sm + net.dsc_off[cur]);
     }
     PH(11);

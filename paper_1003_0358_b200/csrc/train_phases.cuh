@@ -72,14 +72,21 @@ __device__ __forceinline__ void st_flag4(unsigned long long* p, float4 x, int va
 // Weight access: shared memory (resident) or global through L2 only (.cg).
 // Callers pass smem pointers derived from the kernel's extern __shared__
 // array, so RES accesses compile to LDS/STS.128.
-template <bool RES>
-__device__ __forceinline__ float4 ldw4(const float4* p) {
+// Streamed weights (RES = false) bypass L1 (.cg), except the first L1R rows of
+// a thread's block in kernel instances with kFeatL1: those go through L1 (.ca
+// loads, write-back stores), which the kernel otherwise leaves unused (the
+// 28 KB next to the 228 KB shared-memory carve-out; C4's streamed layer 3:
+// +2.5%).  Only this SM reads and writes its rows, and L1 does not survive a
+// launch, so the cached copies stay coherent.
+template <bool RES, int L1R = 0>
+__device__ __forceinline__ float4 ldw4(const float4* p, int row = 0) {
   if constexpr (RES) return *p;
-  else return __ldcg(p);
+  else return row < L1R ? __ldca(p) : __ldcg(p);
 }
-template <bool RES>
-__device__ __forceinline__ void stw4(float4* p, float4 v) {
+template <bool RES, int L1R = 0>
+__device__ __forceinline__ void stw4(float4* p, float4 v, int row = 0) {
   if constexpr (RES) *p = v;
+  else if (row < L1R) __stwb(p, v);
   else __stcg(p, v);
 }
 __device__ __forceinline__ float upd(float w, float d, float x) {  // w + d*x, unfused
@@ -148,7 +155,7 @@ __device__ __forceinline__ float tree_sum(const float* r, int n) {
 // rows over its quads, a transposing warp reduction, a fixed-order sum over
 // the group's warps; one thread per row then applies the scaled tanh, caches
 // t_j and publishes y_j (yslot) and/or keeps it (yown).
-template <bool RES, int CH>
+template <bool RES, int CH, int L1R = 0>
 __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, int gs, int nr,
                                          const float4* __restrict__ v4, float* red, float* tc,
                                          float* yown, unsigned long long* yslot, uint32_t seq,
@@ -182,7 +189,7 @@ __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, 
         float4 w[FB];
 #pragma unroll
         for (int i = 0; i < FB; i++)
-          w[i] = (j4 + i < CH && j4 + i < jn) ? ldw4<RES>(Wg + (j4 + i) * rstep + q)
+          w[i] = (j4 + i < CH && j4 + i < jn) ? ldw4<RES, L1R>(Wg + (j4 + i) * rstep + q, j0 + j4 + i)
                                               : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < FB; i++)
@@ -212,16 +219,16 @@ __device__ __forceinline__ void fwd_rows(const float4* __restrict__ W4, int nq, 
 #undef SUBP
 }
 
-template <bool RES>
+template <bool RES, int L1R = 0>
 __device__ __forceinline__ void fwd_dispatch(const float4* W4, const LayerDev& ly, int nr,
                                              const float4* v4, float* red, float* tc,
                                              float* yown, unsigned long long* yslot,
                                              uint32_t seq, long long* sub = nullptr) {
   const int nq = ly.pitch >> 2, gs = ly.gs;
   switch (ly.CH) {
-    case 4: fwd_rows<RES, 4>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
-    case 8: fwd_rows<RES, 8>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
-    default: fwd_rows<RES, 16>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
+    case 4: fwd_rows<RES, 4, L1R>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
+    case 8: fwd_rows<RES, 8, L1R>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
+    default: fwd_rows<RES, 16, L1R>(W4, nq, gs, nr, v4, red, tc, yown, yslot, seq, sub); break;
   }
 }
 
@@ -229,7 +236,7 @@ __device__ __forceinline__ void fwd_dispatch(const float4* W4, const LayerDev& l
 // weights, published as flag words (bias column excluded, kernels.py:
 // 129-153).  FUSE (streamed layers): the same pass writes the updated weight
 // w + (eta*delta_j)*y_i, so each weight is read once and written once.
-template <bool RES, bool FUSE>
+template <bool RES, bool FUSE, int L1R = 0>
 __device__ __forceinline__ void bwd_partials(float4* W4, int nq, int fi, int gs, int nr,
                                              const float* __restrict__ delta,
                                              const float* __restrict__ dsc,
@@ -248,7 +255,7 @@ __device__ __forceinline__ void bwd_partials(float4* W4, int nq, int fi, int gs,
       float4 w[8];
 #pragma unroll
       for (int i = 0; i < 8; i++)
-        w[i] = i < mp.nj ? ldw4<RES>(Wq + i * rstep) : make_float4(0.f, 0.f, 0.f, 0.f);
+        w[i] = i < mp.nj ? ldw4<RES, L1R>(Wq + i * rstep, i) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int i = 0; i < 8; i++) {
         if (i < mp.nj) {
@@ -265,14 +272,14 @@ __device__ __forceinline__ void bwd_partials(float4* W4, int nq, int fi, int gs,
       }
 #pragma unroll
       for (int i = 0; i < 8; i++)
-        if (i < mp.nj) stw4<RES>(Wq + i * rstep, upd4(w[i], dsc[mp.g + (i << gs)], x));
+        if (i < mp.nj) stw4<RES, L1R>(Wq + i * rstep, upd4(w[i], dsc[mp.g + (i << gs)], x), i);
       continue;
     }
     int j = 0;
     for (; j + 4 <= mp.nj; j += 4) {
       float4 w[4];
 #pragma unroll
-      for (int i = 0; i < 4; i++) w[i] = ldw4<RES>(Wq + (j + i) * rstep);
+      for (int i = 0; i < 4; i++) w[i] = ldw4<RES, L1R>(Wq + (j + i) * rstep, j + i);
 #pragma unroll
       for (int i = 0; i < 4; i++) {
         const int k = mp.g + ((j + i) << gs);
@@ -281,18 +288,18 @@ __device__ __forceinline__ void bwd_partials(float4* W4, int nq, int fi, int gs,
         p.y = fmaf(w[i].y, d, p.y);
         p.z = fmaf(w[i].z, d, p.z);
         p.w = fmaf(w[i].w, d, p.w);
-        if (FUSE) stw4<RES>(Wq + (j + i) * rstep, upd4(w[i], dsc[k], x));
+        if (FUSE) stw4<RES, L1R>(Wq + (j + i) * rstep, upd4(w[i], dsc[k], x), j + i);
       }
     }
     for (; j < mp.nj; j++) {
-      const float4 w = ldw4<RES>(Wq + j * rstep);
+      const float4 w = ldw4<RES, L1R>(Wq + j * rstep, j);
       const int k = mp.g + (j << gs);
       const float d = delta[k];
       p.x = fmaf(w.x, d, p.x);
       p.y = fmaf(w.y, d, p.y);
       p.z = fmaf(w.z, d, p.z);
       p.w = fmaf(w.w, d, p.w);
-      if (FUSE) stw4<RES>(Wq + j * rstep, upd4(w, dsc[k], x));
+      if (FUSE) stw4<RES, L1R>(Wq + j * rstep, upd4(w, dsc[k], x), j);
     }
     if (4 * q < fi) {
       if (gs == 0) st_flag4(pslot + 4 * q, p, fi - 4 * q, seq);
@@ -312,7 +319,7 @@ __device__ __forceinline__ void bwd_partials(float4* W4, int nq, int fi, int gs,
 
 // w_ji += (eta*delta_j) * v_i over the owned rows and every column (bias:
 // v_fi = 1; padding: v = 0 keeps the zeros), same thread mapping.
-template <bool RES>
+template <bool RES, int L1R = 0>
 __device__ __forceinline__ void update_rows(float4* W4, int nq, int gs, int nr,
                                             const float4* __restrict__ v4,
                                             const float* __restrict__ dsc) {
@@ -325,13 +332,13 @@ __device__ __forceinline__ void update_rows(float4* W4, int nq, int gs, int nr,
     for (; j + 4 <= mp.nj; j += 4) {
       float4 w[4];
 #pragma unroll
-      for (int i = 0; i < 4; i++) w[i] = ldw4<RES>(Wq + (j + i) * rstep);
+      for (int i = 0; i < 4; i++) w[i] = ldw4<RES, L1R>(Wq + (j + i) * rstep, j + i);
 #pragma unroll
       for (int i = 0; i < 4; i++)
-        stw4<RES>(Wq + (j + i) * rstep, upd4(w[i], dsc[mp.g + ((j + i) << gs)], x));
+        stw4<RES, L1R>(Wq + (j + i) * rstep, upd4(w[i], dsc[mp.g + ((j + i) << gs)], x), j + i);
     }
     for (; j < mp.nj; j++)
-      stw4<RES>(Wq + j * rstep, upd4(ldw4<RES>(Wq + j * rstep), dsc[mp.g + (j << gs)], x));
+      stw4<RES, L1R>(Wq + j * rstep, upd4(ldw4<RES, L1R>(Wq + j * rstep, j), dsc[mp.g + (j << gs)], x), j);
   }
 }
 
