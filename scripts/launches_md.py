@@ -33,7 +33,7 @@ out = [f"# {TAG} launch list (ncu --metrics gpu__time_duration.sum --clock-contr
 for k, (n, ms) in agg.items():
     out.append(f"| `{k}` | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |")
 out += ["", "`k_train<NRL, RR, RC, RS, FEAT, PROF>` is the persistent on-line BP kernel (register "
-        "plan; FEAT = residency paths compiled in, 1 smem + 2 L2; PROF = 1 is the profiling "
+        "plan; FEAT = residency paths compiled in, 1 smem + 2 L2 + 4 L1-cached streamed rows; PROF = 1 is the profiling "
         "instance the bench launches once for the per-phase profile); one launch trains a whole step of samples. `k_gemm_tanh` + "
         "`k_out_rank` are the validation/evaluation forward; `k_deform` the per-epoch "
         "deformation; `k_pack`/`k_unpack` the reference-layout conversions."]
