@@ -382,7 +382,9 @@ def run_gpu(args) -> dict | None:
     l2 = l2_peak()
     smem_peak = smem_peak_gbs(clk.summary().get("sm_mhz"))
     levels = level_bytes(sizes, dn)
-    t_min = (levels["smem"] / (smem_peak * 1e9) + levels["l2"] / (l2 * 1e9)) if l2 else None
+    # L1 shares the shared-memory datapath (128 B/clk/SM): same peak
+    t_min = ((levels["smem"] + levels["l1"]) / (smem_peak * 1e9) + levels["l2"] / (l2 * 1e9)
+             if l2 else None)
     traffic = profiled_traffic(args.config, n)
     roofline = {
         # the weights live in registers / shared memory / L2 (layer_residency),
@@ -464,8 +466,9 @@ def smem_peak_gbs(sm_mhz) -> float:
 
 def level_bytes(sizes, dn) -> dict:
     """Algorithmic bytes per sample (12 per weight) by the level that serves
-    them in the training kernel: registers, shared memory, L2."""
-    out = {"reg": 0, "smem": 0, "l2": 0}
+    them in the training kernel: registers, shared memory, L1 (the streamed
+    layer's rows the kernel keeps there), L2."""
+    out = {"reg": 0, "smem": 0, "l1": 0, "l2": 0}
     for li, (fi, fo) in enumerate(zip(sizes[:-1], sizes[1:])):
         fi1 = fi + 1
         where = dn.layer_residency[li] if li < len(sizes) - 2 else "smem"  # output tile: smem
@@ -473,6 +476,11 @@ def level_bytes(sizes, dn) -> dict:
             rc = dn.layer_reg_cols[li]
             out["reg"] += 12 * fo * rc
             out["smem"] += 12 * fo * (fi1 - rc)  # the plan's shared-memory tail
+        elif where == "l2" and li < len(dn.layer_l1_rows) and dn.layer_l1_rows[li]:
+            rows = -(-fo // dn.n_ctas)  # rows per CTA
+            part = 12 * fo * fi1 * min(1.0, dn.layer_l1_rows[li] / rows)
+            out["l1"] += int(part)
+            out["l2"] += 12 * fo * fi1 - int(part)
         else:
             out[where] += 12 * fo * fi1
     return out

@@ -78,6 +78,10 @@ int dmlp_net_layer_residency(dmlp_net *net, int32_t *where);
  * (tail_cols); both 0 for smem / L2 layers.  For the hybrid roofline
  * (bench.py: bytes per level / that level's peak). */
 int dmlp_net_layer_regcols(dmlp_net *net, int32_t *reg_cols, int32_t *tail_cols);
+/* Per weight layer: rows per CTA of an L2-streamed layer whose weights the
+ * training kernel serves from L1 (the streamed layer's first rows per thread,
+ * kernel instances with the L1 feature; 0 elsewhere). */
+int dmlp_net_layer_l1rows(dmlp_net *net, int32_t *rows);
 
 /* Pack one layer from the reference layout (fo, fi+1) row-major, bias last
  * (network.py:61-64), host or device pointer, n = fo*(fi+1) floats. */

@@ -41,6 +41,7 @@ SIGNATURES = [
     ("dmlp_net_info", ctypes.c_int, [P, I32P, I32P, I32P, I32P]),
     ("dmlp_net_layer_residency", ctypes.c_int, [P, I32P]),
     ("dmlp_net_layer_regcols", ctypes.c_int, [P, I32P, I32P]),
+    ("dmlp_net_layer_l1rows", ctypes.c_int, [P, I32P]),
     ("dmlp_net_profile", ctypes.c_int, [P, i32]),
     ("dmlp_net_read_profile", ctypes.c_int, [P, I64P]),
     ("dmlp_net_read_profile_all", ctypes.c_int, [P, I64P, i32]),

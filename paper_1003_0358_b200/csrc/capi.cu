@@ -449,6 +449,7 @@ int dmlp_net_create(int device, const int32_t* sizes, int32_t n_sizes, int32_t r
     }
     if (streamed == 1 && l1ok) feat |= kFeatL1;
     if (allpaths) feat = kFeatSmem | kFeatL2;  // sanitizer runs: every residency path
+    net->feat = feat;
     net->train_fn = train_instance(vars[net->variant], feat);
     net->train_fn_prof = vars[net->variant].fn_prof;
   }
@@ -553,6 +554,17 @@ int dmlp_net_layer_regcols(dmlp_net* net, int32_t* reg_cols, int32_t* tail_cols)
     const int fi1 = ly.fi + 1;
     reg_cols[l] = reg ? min(fi1, kThreads * tv.rc) : 0;
     tail_cols[l] = reg ? min(fi1, kThreads * (tv.rc + tv.rs)) - reg_cols[l] : 0;
+  }
+  return DMLP_OK;
+}
+
+int dmlp_net_layer_l1rows(dmlp_net* net, int32_t* rows) {
+  if (!net || !rows) return set_error(DMLP_EINVAL, "null argument");
+  const int H = net->dev.L - 1;
+  for (int l = 0; l < net->dev.L; l++) {
+    const LayerDev& ly = net->dev.ly[l];
+    rows[l] = ((net->feat & kFeatL1) && l >= 1 && l < H && ly.res == kResL2)
+                  ? min(kL1Rows << ly.gs, ly.R) : 0;
   }
   return DMLP_OK;
 }

@@ -77,6 +77,7 @@ struct HostLayer {
 
 struct dmlp_net {
   int device;
+  int feat;       // feature set of the launched training instance (kFeat*)
   int residency;
   int n_sizes;
   int32_t sizes[dmlp::kMaxLayers + 1];

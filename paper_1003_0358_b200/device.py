@@ -69,6 +69,10 @@ class DeviceNet:
         #: the register plan's shared-memory tail (0 unless "reg")
         self.layer_reg_cols = [int(rc[i]) for i in range(len(self.layer_sizes) - 1)]
         self.layer_tail_cols = [int(tc[i]) for i in range(len(self.layer_sizes) - 1)]
+        l1 = (ctypes.c_int32 * (len(self.layer_sizes) - 1))()
+        _lib.check(_lib.lib().dmlp_net_layer_l1rows(self._h, l1), "dmlp_net_layer_l1rows")
+        # rows per CTA of a streamed layer served from L1 (0: none)
+        self.layer_l1_rows = [int(l1[i]) for i in range(len(self.layer_sizes) - 1)]
 
     # -- lifetime ---------------------------------------------------------------
     def close(self):

@@ -19,7 +19,7 @@ out = ["# Round 2 results (one B200, `python bench.py --config Cx`)", "",
        "12 B per weight per sample against the L2 read+write peak measured in the same run (the "
        "weights never live in HBM inside the loop: registers / shared memory / L2); `hybrid` = "
        "SURVEY §8(d) t_min = sum over levels of bytes / level peak (registers free, shared "
-       "memory at 148 x 128 B/clk, L2 measured) divided by the measured sample time; HBM "
+       "memory and L1 at 148 x 128 B/clk, L2 measured) divided by the measured sample time; HBM "
        "fraction kept only as a secondary number. CPU = the reference algorithm (oracle port, "
        "bit-exact with the reference tiled variant) on the box's host cores (C4: 12 s sample, "
        "others 4 s). Hidden-layer residency: s = shared memory, r = register rows, l = L2.", "",

@@ -182,6 +182,21 @@ def test_device_tanhf_matches_libm():
     assert same.all(), x[~same][:5]
 
 
+def test_l1_rows_plan():
+    """The streamed-layer L1 instance is chosen for C4 (layer 3: 5 of its 7 rows
+    per CTA) and nowhere without exactly one streamed layer l >= 1 (C5 streams
+    layer 0; C2 streams nothing)."""
+    from paper_1003_0358_b200.device import DeviceNet
+
+    c4 = DeviceNet((841, 2500, 2000, 1500, 1000, 500, 10))
+    assert c4.layer_residency[3] == "l2" and c4.layer_l1_rows == [0, 0, 0, 5, 0, 0]
+    c4.close()
+    for sizes in ((841,) + (1000,) * 9 + (10,), (841, 1500, 1000, 500, 10)):
+        dn = DeviceNet(sizes)
+        assert not any(dn.layer_l1_rows), (sizes, dn.layer_residency, dn.layer_l1_rows)
+        dn.close()
+
+
 def test_device_tanhf_fast_exhaustive():
     """The training kernel's tanhf (dev_tanhf_fast) on every non-NaN float:
     faithfully rounded (within 1 ulp of the correctly rounded tanh), within
