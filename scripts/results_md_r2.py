@@ -50,5 +50,15 @@ out += ["", f"Deformation (K2): {dfm['imgs_per_s']:,.0f} imgs/s ({dfm['ms_per_ep
         f"Evaluation (K4, C4): {ev['imgs_per_s']:,.0f} imgs/s, {ev['TFLOPs']} TFLOP/s fp32 SIMT.", "",
         "Raw lines: `profiles/r2_bench_*.json`; launch list `profiles/r2_launches.md`; C4 "
         "one-sample timeline `profiles/r2_trace_c4.txt`; GPU tests `profiles/r2_gputest.log`."]
+try:  # the driver-style pair, when captured (scripts: python bench.py; --impl reference)
+    dd = json.load(open("profiles/r2_bench_default.json"))
+    rr = json.load(open("profiles/r2_bench_reference.json"))
+    out += ["", "Driver-style pair on one box (`python bench.py` then `python bench.py --impl "
+            "reference`, `profiles/r2_bench_default.json`, `profiles/r2_bench_reference.json`): "
+            f"ours {dd['value']:,.0f} samples/s device-timed, {dd['e2e']['value']:,.0f} end to end; "
+            f"the reference algorithm on {rr['cpu_baseline']['cores']} host cores "
+            f"{rr['value']:,.1f} samples/s -> e2e ratio {dd['e2e']['value'] / rr['value']:.1f}x."]
+except (OSError, KeyError, ValueError):
+    pass
 open("profiles/r2_results.md", "w").write("\n".join(out) + "\n")
 print("\n".join(out))
