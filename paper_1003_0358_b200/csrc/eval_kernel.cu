@@ -131,6 +131,12 @@ __global__ void __launch_bounds__(GT, 2)
       frag(b ^ 1, 0, 0);
     }
   }
+  float bias[8];  // the bias column of this thread's 8 output columns, loaded once
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const int n = bn + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+    bias[j] = n < N ? __ldg(W + (long long)n * ldw + K) : 0.0f;
+  }
 #pragma unroll
   for (int i = 0; i < 8; i++) {
     const int m = bm + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(GT, 2)
       const int n = bn + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
       if (n >= N) continue;
       const float2 pr = unpack2(acc[i][j >> 1]);
-      const float a = ((j & 1) ? pr.y : pr.x) + __ldg(W + (long long)n * ldw + K);
+      const float a = ((j & 1) ? pr.y : pr.x) + bias[j];
       float t;
       Y[(long long)m * ldy + n] = dev_scaled_tanh(a, &t);
     }
