@@ -55,39 +55,50 @@ template <bool VEC>
 __global__ void __launch_bounds__(GT, 2)
     k_gemm_tanh(const float* __restrict__ X, long long ldx, const float* __restrict__ W, int ldw,
                 int M, int N, int K, float* __restrict__ Y, int ldy) {
-  constexpr int KB = 8;  // k per smem tile
+#ifndef DMLP_EVAL_KB
+#define DMLP_EVAL_KB 16
+#endif
+  constexpr int KB = DMLP_EVAL_KB;  // k per smem tile
+  constexpr int NL = KB / 8;        // float4 loads per thread per matrix per tile
   __shared__ __align__(16) float As[2][KB][BM];
   __shared__ __align__(16) float Bs[2][KB][BN];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
-  const int lr = tid & 127, lk = (tid >> 7) * 4;  // loader: row, first of 4 k
+  const int lr = tid & 127, lk = (tid >> 7) * 4;  // loader: row, first of 4 k (+ 8 r)
   const bool am = bm + lr < M, bnv = bn + lr < N;
   const float* xa = X + (long long)(am ? bm + lr : 0) * ldx;
   const float* wb = W + (long long)(bnv ? bn + lr : 0) * ldw;
-  float4 ra, rb;
+  float4 ra[NL], rb[NL];
   auto load = [&](int k0) {
-    const int kb = k0 + lk;
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (VEC && kb + 4 <= K) {
-      ra = am ? *reinterpret_cast<const float4*>(xa + kb) : z;
-      rb = bnv ? __ldg(reinterpret_cast<const float4*>(wb + kb)) : z;
-    } else {
-      ra.x = (am && kb < K) ? xa[kb] : 0.f;
-      ra.y = (am && kb + 1 < K) ? xa[kb + 1] : 0.f;
-      ra.z = (am && kb + 2 < K) ? xa[kb + 2] : 0.f;
-      ra.w = (am && kb + 3 < K) ? xa[kb + 3] : 0.f;
-      rb.x = (bnv && kb < K) ? __ldg(wb + kb) : 0.f;
-      rb.y = (bnv && kb + 1 < K) ? __ldg(wb + kb + 1) : 0.f;
-      rb.z = (bnv && kb + 2 < K) ? __ldg(wb + kb + 2) : 0.f;
-      rb.w = (bnv && kb + 3 < K) ? __ldg(wb + kb + 3) : 0.f;
+#pragma unroll
+    for (int r = 0; r < NL; r++) {
+      const int kb = k0 + lk + 8 * r;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (VEC && kb + 4 <= K) {
+        ra[r] = am ? *reinterpret_cast<const float4*>(xa + kb) : z;
+        rb[r] = bnv ? __ldg(reinterpret_cast<const float4*>(wb + kb)) : z;
+      } else {
+        ra[r].x = (am && kb < K) ? xa[kb] : 0.f;
+        ra[r].y = (am && kb + 1 < K) ? xa[kb + 1] : 0.f;
+        ra[r].z = (am && kb + 2 < K) ? xa[kb + 2] : 0.f;
+        ra[r].w = (am && kb + 3 < K) ? xa[kb + 3] : 0.f;
+        rb[r].x = (bnv && kb < K) ? __ldg(wb + kb) : 0.f;
+        rb[r].y = (bnv && kb + 1 < K) ? __ldg(wb + kb + 1) : 0.f;
+        rb[r].z = (bnv && kb + 2 < K) ? __ldg(wb + kb + 2) : 0.f;
+        rb[r].w = (bnv && kb + 3 < K) ? __ldg(wb + kb + 3) : 0.f;
+      }
     }
   };
   auto store = [&](int b) {
-    As[b][lk + 0][lr] = ra.x; As[b][lk + 1][lr] = ra.y;
-    As[b][lk + 2][lr] = ra.z; As[b][lk + 3][lr] = ra.w;
-    Bs[b][lk + 0][lr] = rb.x; Bs[b][lk + 1][lr] = rb.y;
-    Bs[b][lk + 2][lr] = rb.z; Bs[b][lk + 3][lr] = rb.w;
+#pragma unroll
+    for (int r = 0; r < NL; r++) {
+      const int k = lk + 8 * r;
+      As[b][k + 0][lr] = ra[r].x; As[b][k + 1][lr] = ra[r].y;
+      As[b][k + 2][lr] = ra[r].z; As[b][k + 3][lr] = ra[r].w;
+      Bs[b][k + 0][lr] = rb[r].x; Bs[b][k + 1][lr] = rb[r].y;
+      Bs[b][k + 2][lr] = rb[r].z; Bs[b][k + 3][lr] = rb[r].w;
+    }
   };
   unsigned long long acc[8][4];  // (acc[i][2p], acc[i][2p+1]) packed for FFMA2
 #pragma unroll
