@@ -53,7 +53,7 @@ out += ["", f"Deformation (K2): {dfm['imgs_per_s']:,.0f} imgs/s ({dfm['ms_per_ep
 try:  # the driver-style pair, when captured (scripts: python bench.py; --impl reference)
     dd = json.load(open("profiles/r2_bench_default.json"))
     rr = json.load(open("profiles/r2_bench_reference.json"))
-    out += ["", "Driver-style pair on one box (`python bench.py` then `python bench.py --impl "
+    out += ["", "Driver-style pair (`python bench.py` and `python bench.py --impl "
             "reference`, `profiles/r2_bench_default.json`, `profiles/r2_bench_reference.json`): "
             f"ours {dd['value']:,.0f} samples/s device-timed, {dd['e2e']['value']:,.0f} end to end; "
             f"the reference algorithm on {rr['cpu_baseline']['cores']} host cores "
