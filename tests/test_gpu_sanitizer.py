@@ -57,6 +57,20 @@ def test_train_kernel_sanitizer(tmp_path, tool, feat, sizes):
     assert "ERROR SUMMARY: 0 errors" in out or "0 hazards" in out, out[-3000:]
 
 
+@pytest.mark.parametrize("tool", ["synccheck", "racecheck", "memcheck"])
+def test_train_kernel_l1_instance_sanitizer(tmp_path, tool):
+    """The headline net's auto plan runs the L1-feature instance (layer 3's
+    first rows per thread through L1): two samples under each tool."""
+    script = tmp_path / "case.py"
+    script.write_text(CASE)
+    p = subprocess.run([_sanitizer(), "--tool", tool, "--print-limit", "4", "--error-exitcode", "9",
+                        sys.executable, str(script), "841,2500,2000,1500,1000,500,10", "2", "0"],
+                       capture_output=True, text=True, timeout=600)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0 and "ok " in out, out[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "0 hazards" in out, out[-3000:]
+
+
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
 def test_deform_eval_sanitizer(tool):
     """memcheck / racecheck of the deformation (4 images per CTA, ragged last
