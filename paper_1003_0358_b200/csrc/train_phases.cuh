@@ -434,17 +434,22 @@ template <int RR, int RC, int RS>
 __device__ __forceinline__ void reg_partials(const float (&w)[RR][RC], float* tail, int fi,
                                              int nr, const float* __restrict__ delta,
                                              unsigned long long* pslot, uint32_t seq) {
-  float d[RR];
+  // all RC + RS column chains advance together (k ascending in each, the same
+  // sums as one chain at a time), then the stores
+  float p[RC + RS];
 #pragma unroll
-  for (int k = 0; k < RR; k++) d[k] = k < nr ? delta[k] : 0.0f;
+  for (int m = 0; m < RC + RS; m++) p[m] = 0.0f;
+#pragma unroll
+  for (int k = 0; k < RR; k++) {
+    const float d = k < nr ? delta[k] : 0.0f;
+#pragma unroll
+    for (int m = 0; m < RC + RS; m++)
+      p[m] = fmaf(m < RC ? w[k][m < RC ? m : 0] : tail_at<RR, RS>(tail, m - RC, k), d, p[m]);
+  }
 #pragma unroll
   for (int m = 0; m < RC + RS; m++) {
     const int c = threadIdx.x + kThreads * m;
-    float p = 0.0f;
-#pragma unroll
-    for (int k = 0; k < RR; k++)
-      p = fmaf(m < RC ? w[k][m < RC ? m : 0] : tail_at<RR, RS>(tail, m - RC, k), d[k], p);
-    if (c < fi) st_flag(pslot + c, p, seq);
+    if (c < fi) st_flag(pslot + c, p[m], seq);
   }
 }
 
