@@ -227,3 +227,26 @@ def test_bench_gpus_flag_relaunches_under_torchrun():
     line = json.loads(lines[0])
     assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+
+
+def test_bench_level_bytes_split():
+    """bench.py's hybrid roofline: 12 B per weight by the level that serves it --
+    register columns and the register plan's smem tail, smem layers, and a
+    streamed layer split between L1 (its L1-served rows per CTA) and L2; the
+    output tile counts as smem.  Every weight is counted once."""
+    import importlib.util
+    import types
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    sizes = (841, 2500, 2000, 1500, 1000, 500, 10)
+    dn = types.SimpleNamespace(
+        layer_residency=["smem", "reg", "smem", "l2", "smem", "smem"],
+        layer_reg_cols=[0, 2048, 0, 0, 0, 0], layer_l1_rows=[0, 0, 0, 5, 0, 0], n_ctas=148)
+    lv = bench.level_bytes(sizes, dn)
+    W = sum((i + 1) * o for i, o in zip(sizes[:-1], sizes[1:]))
+    assert sum(lv.values()) == 12 * W
+    assert lv["reg"] == 12 * 2000 * 2048
+    l3 = 12 * 1000 * 1501
+    assert lv["l1"] == int(l3 * 5 / 7) and lv["l2"] == l3 - lv["l1"]
