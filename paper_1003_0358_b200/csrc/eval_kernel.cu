@@ -265,7 +265,13 @@ static int run_eval(dmlp_net* net, const float* x, long long n, float* out, cons
   const int L = net->dev.L;
   int maxld = net->hl[0].pitch;  // activation row stride = input pitch of the consuming layer
   for (int l = 1; l < L; l++) maxld = maxld > net->hl[l].pitch ? maxld : net->hl[l].pitch;
-  const long long chunk = n < 16384 ? n : 16384;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, net->device);
+  // a full chunk is one BM-row tile per SM: every layer's grid is then (column
+  // tiles) x sms CTAs, whole waves at 2 CTAs per SM for an even number of
+  // column tiles (C4: 20/16/12/8/4), where 16384 rows left partial last waves
+  const long long cmax = (long long)BM * sms;
+  const long long chunk = n < cmax ? n : cmax;
   if (int rc = ensure_act(net, (size_t)chunk, maxld)) return rc;
   const HostLayer& ho = net->hl[L - 1];
   const int osmem = (ho.fo * ho.pitch + 128) * (int)sizeof(float);
@@ -273,8 +279,6 @@ static int run_eval(dmlp_net* net, const float* x, long long n, float* out, cons
           cudaFuncSetAttribute(k_out_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, osmem),
           "cudaFuncSetAttribute"))
     return rc;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, net->device);
   if (int rc = net_begin(net, st)) return rc;
   for (long long m0 = 0; m0 < n; m0 += chunk) {
     const int M = (int)((n - m0) < chunk ? (n - m0) : chunk);
