@@ -357,3 +357,31 @@ def test_train_epoch_strided_rows_bit_identical(golden, ldx):
     assert wrongs[0] == wrongs[1]
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
     assert np.isfinite(outs[1]).all()  # the NaN padding was never read
+
+
+def test_profile_per_cta_readout(golden):
+    """In-kernel profile: the summed phase cycles are positive and cover the
+    exchange waits; the per-CTA readout gives every CTA its own SM (one CTA
+    per SM in the cooperative launch) and per-CTA slots that sum to the
+    totals."""
+    import torch
+
+    from paper_1003_0358_b200.device import DeviceNet
+
+    sizes = (841, 1000, 500, 10)
+    g = golden("train")
+    x = torch.from_numpy(g["deformed"].reshape(64, -1)).cuda()
+    lab = torch.from_numpy(g["labels"]).cuda()
+    dn = DeviceNet(sizes)
+    dn.set_layers(O.init_layers(3, sizes))
+    dn.profile(True)
+    wrong = torch.zeros((), dtype=torch.int64, device="cuda")
+    dn.train_epoch(x, lab, None, 1e-3, wrong)
+    sm, slots = dn.read_profile_cta()
+    assert sm.shape == (dn.n_ctas,) and len(set(sm.tolist())) == dn.n_ctas
+    assert (sm >= 0).all() and (slots[:, 0] > 0).all()  # loop cycles of every CTA
+    dn.train_epoch(x, lab, None, 1e-3, wrong)
+    tot = dn.read_profile()
+    assert tot["loop"] > 0 and 0.0 < tot["exchange_fraction"] < 1.0
+    dn.profile(False)
+    dn.close()
